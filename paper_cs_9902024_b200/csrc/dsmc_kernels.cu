@@ -1,0 +1,1091 @@
+// dsmc_kernels.cu -- sm_100a kernels of the batched unsteady-DSMC step.
+//
+// Step = inner loop (1) of PAPER.md Fig. 1 (lines 95-110), batched over the
+// n independent runs of the outer loop (2) (lines 112-115):
+//
+//   k_zero          counts <- 0                                   (LCR prep)
+//   k_inflow_count  per (run, face cell): kept inflow particles   Generation
+//   k_inflow_emit   append them at each run's tail, key, count    Generation
+//   k_motion        free flight + surfaces, cell key, count       Motion, Enumeration
+//   k_step_mid      store lengths, reorder flags                  (control)
+//   k_scan_*        exclusive scan of counts -> starts            Indexing
+//   k_scatter       LCR[start + rank] = particle                  Indexing
+//   k_collide       per cell: canonical order, NTC, Sampling,     Interaction, Sampling
+//                   (sigma g)_max, physical reorder
+//   k_step_end      parity/length after reorder, step++           (control)
+//
+// The paper's "Indexing ... can not be parallelized, so it is performed by one
+// processor" is replaced by a parallel counting sort; the
+// within-cell order (ascending store index, reading R11) is restored inside
+// k_collide, which stages each tile of cells in shared memory.
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <curand_kernel.h>
+
+#include "dsmc_device.cuh"
+#include "dsmc_kernels.h"
+
+namespace dsmc {
+
+constexpr unsigned FULL = 0xFFFFFFFFu;
+
+// ====================================================================== util
+__global__ void k_zero(uint32_t* __restrict__ a, int64_t n) {
+  const int64_t n4 = n >> 2;
+  uint4* a4 = reinterpret_cast<uint4*>(a);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride)
+    a4[i] = make_uint4(0, 0, 0, 0);
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) a[n4 * 4 + threadIdx.x] = 0;
+}
+
+__global__ void k_fill_f32(float* __restrict__ a, int64_t n, float v) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) a[i] = v;
+}
+
+// ==================================================================== scan
+// three-phase exclusive scan of uint32 counts (tile = 2048 elements / block)
+constexpr int SCAN_T = 256, SCAN_PER = 8, SCAN_TILE = SCAN_T * SCAN_PER;
+
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t t = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(FULL, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) s_warp[lane] = t;  // inclusive warp prefix
+  }
+  __syncthreads();
+  total = s_warp[nw - 1];
+  const uint32_t wpre = wid ? s_warp[wid - 1] : 0;
+  __syncthreads();
+  return wpre + x - v;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_reduce(const uint32_t* __restrict__ a, int64_t L,
+                                                        uint32_t* __restrict__ part) {
+  __shared__ uint32_t s_warp[32];
+  const int64_t b = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_PER;
+  uint32_t s = 0;
+  if (b + SCAN_PER <= L) {
+    const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(a + b));
+    const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(a + b + 4));
+    s = v0.x + v0.y + v0.z + v0.w + v1.x + v1.y + v1.z + v1.w;
+  } else {
+    for (int i = 0; i < SCAN_PER; i++) if (b + i < L) s += a[b + i];
+  }
+  uint32_t total;
+  block_excl_scan(s, s_warp, total);
+  if (threadIdx.x == 0) part[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_partials(uint32_t* __restrict__ part, int64_t nb) {
+  __shared__ uint32_t s_warp[32];
+  const int64_t per = (nb + blockDim.x - 1) / blockDim.x;
+  const int64_t b = (int64_t)threadIdx.x * per;
+  uint32_t s = 0;
+  for (int64_t i = 0; i < per; i++) if (b + i < nb) s += part[b + i];
+  uint32_t total;
+  uint32_t run = block_excl_scan(s, s_warp, total);
+  for (int64_t i = 0; i < per; i++)
+    if (b + i < nb) { uint32_t v = part[b + i]; part[b + i] = run; run += v; }
+  if (threadIdx.x == 0) part[nb] = total;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_down(uint32_t* __restrict__ a, int64_t L,
+                                                      const uint32_t* __restrict__ part) {
+  __shared__ uint32_t s_warp[32];
+  const int64_t b = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_PER;
+  uint32_t v[SCAN_PER];
+  const bool full = b + SCAN_PER <= L;
+  if (full) {
+    const uint4 v0 = *reinterpret_cast<const uint4*>(a + b);
+    const uint4 v1 = *reinterpret_cast<const uint4*>(a + b + 4);
+    v[0] = v0.x; v[1] = v0.y; v[2] = v0.z; v[3] = v0.w; v[4] = v1.x; v[5] = v1.y; v[6] = v1.z; v[7] = v1.w;
+  } else {
+    for (int i = 0; i < SCAN_PER; i++) v[i] = b + i < L ? a[b + i] : 0;
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_PER; i++) s += v[i];
+  uint32_t total;
+  uint32_t run = block_excl_scan(s, s_warp, total) + part[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < SCAN_PER; i++) { const uint32_t t = v[i]; v[i] = run; run += t; }
+  if (full) {
+    *reinterpret_cast<uint4*>(a + b) = make_uint4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<uint4*>(a + b + 4) = make_uint4(v[4], v[5], v[6], v[7]);
+  } else {
+    for (int i = 0; i < SCAN_PER; i++) if (b + i < L) a[b + i] = v[i];
+  }
+}
+
+// ==================================================================== fill
+__device__ __forceinline__ int fill_region(const Prm& P, int64_t c, int32_t ic[3]) {
+  ic[0] = (int32_t)(c % P.nx);
+  ic[1] = (int32_t)((c / P.nx) % P.ny);
+  ic[2] = (int32_t)(c / ((int64_t)P.nx * P.ny));
+  for (int k = 0; k < P.n_fill; k++) {
+    bool in = true;
+    for (int a = 0; a < 3; a++) in = in && ic[a] >= P.fill_lo[k][a] && ic[a] < P.fill_hi[k][a];
+    if (in) return k;
+  }
+  return -1;
+}
+
+__global__ void k_fill_count(Prm P) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P.Nc) return;
+  int32_t ic[3];
+  const int k = fill_region(P, c, ic);
+  P.cell[c] = k < 0 ? 0u : (uint32_t)P.fill_ppc[k];
+}
+
+// warp per (cell, run); store order (cell, k) (reading R7)
+__global__ void k_fill_emit(Prm P) {
+  const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int r = blockIdx.y, lane = threadIdx.x & 31;
+  if (c >= P.Nc) return;
+  int32_t ic[3];
+  const int k = fill_region(P, c, ic);
+  if (k < 0) return;
+  const uint32_t off = P.cell[c];
+  const int ppc = P.fill_ppc[k];
+  const uint2 key = run_key(P, r);
+  const int64_t base = (int64_t)r * P.stride;
+  const double sq = P.fill_sqrtT[k];
+  for (int q = lane; q < ppc; q += 32) {
+    const int64_t i = (int64_t)off + q;
+    if (i >= P.cap) { latch(P, ST_CAP); continue; }
+    const uint4 w = draw(key, (uint32_t)c, FILL_STEP, TAG_FILL, (uint32_t)q, 0);
+    const uint4 u = draw(key, (uint32_t)c, FILL_STEP, TAG_FILL, (uint32_t)q, 1);
+    const uint32_t ww[3] = {w.x, w.y, w.z};
+    for (int a = 0; a < 3; a++) parr(P, 0, a)[base + i] = a < P.dim ? place(ic[a], ww[a]) : 0.0f;
+    double n1, n2, n3, n4;
+    box_muller(u.x, u.y, n1, n2);
+    box_muller(u.z, u.w, n3, n4);
+    parr(P, 0, 3)[base + i] = (float)(P.fill_u[k][0] + sq * n1);
+    parr(P, 0, 4)[base + i] = (float)(P.fill_u[k][1] + sq * n2);
+    parr(P, 0, 5)[base + i] = (float)(P.fill_u[k][2] + sq * n3);
+  }
+}
+
+// per run: lengths and control reset after a fill
+__global__ void k_fill_finish(Prm P) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == 0) { *P.ctl.step = 0; }
+  if (r < P.n_slots) P.ctl.slot_done[r] = 0;
+  if (r >= P.R) return;
+  int32_t ic[3];
+  const int k = fill_region(P, P.Nc - 1, ic);
+  int64_t total = (int64_t)P.cell[P.Nc - 1] + (k < 0 ? 0 : P.fill_ppc[k]);
+  if (total > P.cap) total = P.cap;
+  P.ctl.n_store[r] = total;
+  P.ctl.live[r] = total;
+  P.ctl.psteps[r] = 0;
+  P.ctl.parity[r] = 0;
+  P.ctl.reorder[r] = 0;
+  P.ctl.inserted[r] = 0;
+  for (int q = 0; q < 4; q++) P.ctl.counters[r * 4 + q] = 0;
+}
+
+// ============================================================== Generation
+// one inflow particle (reading R8): ghost buffer (drifting Maxwellian, flies
+// dt from behind the face) or effusion (Rayleigh normal speed, flies u dt)
+__device__ __forceinline__ bool gen_particle(const Prm& P, uint2 key, int f, uint32_t s, uint32_t k, float pos[3],
+                                             float vel[3]) {
+  const uint4 a = draw(key, (uint32_t)f, s, TAG_INFLOW_PARTICLE, k, 0);
+  const uint4 b = draw(key, (uint32_t)f, s, TAG_INFLOW_PARTICLE, k, 1);
+  double n1, n2, n3, n4;
+  box_muller(b.x, b.y, n1, n2);
+  box_muller(b.z, b.w, n3, n4);
+  const double sq = P.sqrt_inflowT;
+  float x0[3], tau;
+  x0[1] = place(P.face_j[f], a.y);
+  x0[2] = place(P.face_k[f], a.z);
+  if (P.inflow_kind == 1) {
+    x0[0] = -(P.ghost_w_f * (float)u_oc_d(a.x));
+    vel[0] = (float)(P.inflow_U + sq * n1);
+    vel[1] = (float)(0.0 + sq * n2);
+    vel[2] = (float)(0.0 + sq * n3);
+    tau = P.dt_f;
+  } else {
+    x0[0] = 0.0f;
+    vel[0] = (float)(sq * sqrt(-2.0 * log(u_oc_d(a.w))));
+    vel[1] = (float)(0.0 + sq * n1);
+    vel[2] = (float)(0.0 + sq * n2);
+    tau = u_co(a.x) * P.dt_f;
+  }
+  bool kept = true;
+#pragma unroll
+  for (int d = 0; d < 3; d++) {
+    pos[d] = d < P.dim ? fmaf(vel[d], tau, x0[d]) : 0.0f;
+    if (d < P.dim && !(pos[d] >= 0.0f && pos[d] <= (float)axis_n(P, d))) kept = false;
+  }
+  return kept;
+}
+
+__device__ __forceinline__ int64_t inflow_n(const Prm& P, uint2 key, int f, uint32_t s) {
+  if (P.inflow_kind == 2) return P.inflow_count;
+  const uint4 w = draw(key, (uint32_t)f, s, TAG_INFLOW_COUNT, 0, 0);
+  return (int64_t)floor(P.ghost_x + u_co_d(w.x));
+}
+
+// warp per (run, face cell): number of kept particles
+__global__ void k_inflow_count(Prm P) {
+  const int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int r = blockIdx.y, lane = threadIdx.x & 31;
+  if (f >= P.n_face) return;
+  const uint2 key = run_key(P, r);
+  const uint32_t s = *P.ctl.step;
+  const int64_t cnt = inflow_n(P, key, f, s);
+  int kept = 0;
+  for (int64_t k0 = 0; k0 < cnt; k0 += 32) {
+    bool kp = false;
+    if (k0 + lane < cnt) {
+      float pos[3], vel[3];
+      kp = gen_particle(P, key, f, s, (uint32_t)(k0 + lane), pos, vel);
+    }
+    kept += __popc(__ballot_sync(FULL, kp));
+  }
+  if (lane == 0) P.face_kept[(int64_t)r * P.n_face + f] = kept;
+}
+
+// warp per (run, face cell): append in (face, k) order at the run's tail
+__global__ void k_inflow_emit(Prm P) {
+  const int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int r = blockIdx.y, lane = threadIdx.x & 31;
+  if (f >= P.n_face) return;
+  const int32_t* kept_r = P.face_kept + (int64_t)r * P.n_face;
+  uint32_t pre = 0;
+  for (int q = lane; q < f; q += 32) pre += kept_r[q];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(FULL, pre, o);
+  const uint2 key = run_key(P, r);
+  const uint32_t s = *P.ctl.step;
+  const int64_t n0 = P.ctl.n_store[r];
+  const int h = P.ctl.parity[r];
+  const int64_t base = (int64_t)r * P.stride;
+  const int64_t cnt = inflow_n(P, key, f, s);
+  int64_t pos_out = n0 + pre;
+  for (int64_t k0 = 0; k0 < cnt; k0 += 32) {
+    float pos[3], vel[3];
+    bool kp = false;
+    if (k0 + lane < cnt) kp = gen_particle(P, key, f, s, (uint32_t)(k0 + lane), pos, vel);
+    const unsigned bal = __ballot_sync(FULL, kp);
+    if (kp) {
+      const int64_t i = pos_out + __popc(bal & ((1u << lane) - 1u));
+      if (i < P.cap) {
+        for (int a = 0; a < 3; a++) {
+          parr(P, h, a)[base + i] = pos[a];
+          parr(P, h, 3 + a)[base + i] = vel[a];
+        }
+        int32_t ic[3] = {0, 0, 0};
+        for (int a = 0; a < P.dim; a++) {
+          int32_t c = (int32_t)floorf(pos[a]);
+          const int32_t L = axis_n(P, a);
+          ic[a] = c > L - 1 ? L - 1 : c;
+        }
+        const uint32_t kk = (uint32_t)r * (uint32_t)P.Nc + (uint32_t)(ic[0] + P.nx * (ic[1] + P.ny * ic[2]));
+        P.key[base + i] = kk;
+        atomicAdd(&P.cell[kk], 1u);
+      } else {
+        latch(P, ST_CAP);
+      }
+    }
+    pos_out += __popc(bal);
+  }
+  if (f == P.n_face - 1 && lane == 0) {
+    int64_t total = pos_out - n0;
+    if (n0 + total > P.cap) total = P.cap - n0;
+    P.ctl.inserted[r] = (int32_t)total;
+    P.ctl.counters[r * 4 + 0] += (unsigned long long)total;
+  }
+}
+
+// ================================================================= Motion
+// Full-accommodation diffuse re-emission (reading R10): Rayleigh normal speed
+// into the domain, N(0, T) tangential components, in fp64 then rounded.
+__device__ __forceinline__ void diffuse(uint2 key, uint32_t idx, uint32_t s, uint32_t b, int a, int sign, double sq,
+                                        float v[3]) {
+  const uint4 w = draw(key, idx, s, TAG_WALL, b, 0);
+  const double vn = sq * sqrt(-2.0 * log(u_oc_d(w.x)));
+  double t1, t2;
+  box_muller(w.y, w.z, t1, t2);
+  const int c1 = a == 0 ? 1 : 0, c2 = a == 2 ? 1 : 2;
+  v[a] = (float)(sign > 0 ? vn : -vn);
+  v[c1] = (float)(0.0 + sq * t1);
+  v[c2] = (float)(0.0 + sq * t2);
+}
+
+// Motion with surface interaction (reading R10).  Returns
+// true if the particle left the domain.  EV = the problem has event surfaces
+// (diffuse / outflow / inflow faces or the plate).
+template <int D, bool EV>
+__device__ __forceinline__ bool move_one(const Prm& P, uint2 key, uint32_t idx, uint32_t s, float x[3], float v[3],
+                                         bool& vchg) {
+  float tau = P.dt_f;
+  if (EV) {
+    for (int b = 0;; b++) {
+      float x1[3] = {x[0], x[1], x[2]};
+#pragma unroll
+      for (int a = 0; a < D; a++) x1[a] = fmaf(v[a], tau, x[a]);
+      int ev = -1;
+      float tbest = __int_as_float(0x7f800000);
+#pragma unroll
+      for (int a = 0; a < D; a++) {
+#pragma unroll
+        for (int f = 0; f < 2; f++) {
+          const int bc = P.bc[2 * a + f];
+          if (bc == BC_SPECULAR || bc == BC_PERIODIC) continue;
+          const float L = f ? (float)axis_n(P, a) : 0.0f;
+          const bool crossed = f ? (x1[a] > L) : (x1[a] < L);
+          if (crossed) {
+            const float t = (L - x[a]) / v[a];
+            if (t < tbest) { tbest = t; ev = 2 * a + f; }
+          }
+        }
+      }
+      bool s0 = false;
+      if (D == 2 && P.plate_on) {
+        const int pa = P.plate_axis, qa = P.plate_span_axis;
+        const float pc = P.plate_pos;
+        s0 = x[pa] >= pc;
+        const bool s1 = x1[pa] >= pc;
+        if (s0 != s1) {
+          const float t = (pc - x[pa]) / v[pa];
+          const float xq = fmaf(v[qa], t, x[qa]);
+          if (xq >= P.plate_lo && xq <= P.plate_hi && t < tbest) { tbest = t; ev = 6; }
+        }
+      }
+      if (ev < 0) {
+#pragma unroll
+        for (int a = 0; a < D; a++) x[a] = x1[a];
+        break;
+      }
+      const float t = tbest < tau ? tbest : tau;
+      if (ev < 6) {
+        const int a = ev >> 1, f = ev & 1, bc = P.bc[ev];
+        if (bc == BC_OUTFLOW || bc == BC_INFLOW) return true;
+#pragma unroll
+        for (int c = 0; c < D; c++) if (c != a) x[c] = fmaf(v[c], t, x[c]);
+        x[a] = f ? (float)axis_n(P, a) : 0.0f;
+        if (D == 3 && P.orifice_on && a == 0 && f == 0) {
+          int32_t j = (int32_t)floorf(x[1]), k = (int32_t)floorf(x[2]);
+          j = j < 0 ? 0 : (j > P.ny - 1 ? P.ny - 1 : j);
+          k = k < 0 ? 0 : (k > P.nz - 1 ? P.nz - 1 : k);
+          if (P.open_face[(int64_t)k * P.ny + j]) return true;
+        }
+        if (b == MAX_BOUNCE) { latch(P, ST_BOUNCE); break; }
+        diffuse(key, idx, s, (uint32_t)b, a, f ? -1 : 1, P.sqrt_bcT[ev], v);
+      } else {
+        const int pa = P.plate_axis;
+        const float pc = P.plate_pos;
+#pragma unroll
+        for (int c = 0; c < D; c++) if (c != pa) x[c] = fmaf(v[c], t, x[c]);
+        x[pa] = s0 ? pc : nextafterf(pc, -__int_as_float(0x7f800000));
+        if (b == MAX_BOUNCE) { latch(P, ST_BOUNCE); break; }
+        diffuse(key, idx, s, (uint32_t)b, pa, s0 ? 1 : -1, P.sqrt_plateT, v);
+      }
+      vchg = true;
+      tau = tau - t;
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < D; a++) x[a] = fmaf(v[a], tau, x[a]);
+  }
+#pragma unroll
+  for (int a = 0; a < D; a++) {
+    const float L = (float)axis_n(P, a);
+    if (P.bc[2 * a] == BC_PERIODIC) {
+      if (x[a] >= L) x[a] = x[a] - L;
+      else if (x[a] < 0.0f) { x[a] = x[a] + L; if (x[a] >= L) x[a] = 0.0f; }
+    } else {
+      if (x[a] < 0.0f && P.bc[2 * a] == BC_SPECULAR) { x[a] = -x[a]; v[a] = -v[a]; vchg = true; }
+      else if (x[a] > L && P.bc[2 * a + 1] == BC_SPECULAR) { x[a] = 2.0f * L - x[a]; v[a] = -v[a]; vchg = true; }
+    }
+  }
+  return false;
+}
+
+// Enumeration (reading R11): floor per axis, clamped.
+template <int D>
+__device__ __forceinline__ uint32_t enumerate(const Prm& P, const float x[3], const float v[3], uint32_t kbase) {
+  int32_t ic[3] = {0, 0, 0};
+#pragma unroll
+  for (int a = 0; a < D; a++) {
+    const int32_t L = axis_n(P, a);
+    if (!(x[a] >= 0.0f && x[a] <= (float)L)) latch(P, ST_INDEX);
+    int32_t c = x[a] >= 0.0f ? (int32_t)floorf(x[a]) : 0;
+    ic[a] = c > L - 1 ? L - 1 : c;
+  }
+  if (!(isfinite(v[0]) && isfinite(v[1]) && isfinite(v[2]))) latch(P, ST_NONFINITE);
+  return kbase + (uint32_t)(ic[0] + P.nx * (ic[1] + P.ny * ic[2]));
+}
+
+// persistent over (run = blockIdx.y, 4 consecutive particles per lane);
+// mode 0: move + enumerate, mode 1: enumerate only (explicit Sampling)
+template <int D, bool EV>
+__global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
+  const int r = blockIdx.y, lane = threadIdx.x & 31;
+  const int64_t n = P.ctl.n_store[r];
+  const int h = P.ctl.parity[r];
+  const int64_t base = (int64_t)r * P.stride;
+  float* X[3];
+  float* V[3];
+#pragma unroll
+  for (int a = 0; a < 3; a++) { X[a] = parr(P, h, a) + base; V[a] = parr(P, h, 3 + a) + base; }
+  uint32_t* K = P.key + base;
+  const uint2 key = run_key(P, r);
+  const uint32_t s = (uint32_t)*P.ctl.step;
+  const uint32_t kbase = (uint32_t)r * (uint32_t)P.Nc;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  uint32_t removed = 0;
+  for (int64_t i0w = w * 128; i0w < n; i0w += nw * 128) {
+    const int64_t i0 = i0w + lane * 4;
+    float x[4][3], v[4][3];
+    const bool full = i0 + 4 <= n;
+    if (full) {
+#pragma unroll
+      for (int a = 0; a < D; a++) {
+        const float4 q = *reinterpret_cast<const float4*>(X[a] + i0);
+        x[0][a] = q.x; x[1][a] = q.y; x[2][a] = q.z; x[3][a] = q.w;
+      }
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        const float4 q = *reinterpret_cast<const float4*>(V[a] + i0);
+        v[0][a] = q.x; v[1][a] = q.y; v[2][a] = q.z; v[3][a] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const bool in = i0 + j < n;
+#pragma unroll
+        for (int a = 0; a < D; a++) x[j][a] = in ? X[a][i0 + j] : DEAD_X;
+#pragma unroll
+        for (int a = 0; a < 3; a++) v[j][a] = in ? V[a][i0 + j] : 0.0f;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+#pragma unroll
+      for (int a = D; a < 3; a++) x[j][a] = 0.0f;
+    uint32_t kk[4];
+    bool vchg = false, xchg = false;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      if (x[j][0] < -1.0e29f) { kk[j] = DEAD_KEY; continue; }
+      if (mode == 0) {
+        xchg = true;
+        if (move_one<D, EV>(P, key, (uint32_t)(i0 + j), s, x[j], v[j], vchg)) {
+          x[j][0] = DEAD_X;
+          kk[j] = DEAD_KEY;
+          removed++;
+          continue;
+        }
+      }
+      kk[j] = enumerate<D>(P, x[j], v[j], kbase);
+    }
+    if (full) {
+      if (xchg) {
+#pragma unroll
+        for (int a = 0; a < D; a++)
+          *reinterpret_cast<float4*>(X[a] + i0) = make_float4(x[0][a], x[1][a], x[2][a], x[3][a]);
+      }
+      if (vchg) {
+#pragma unroll
+        for (int a = 0; a < 3; a++)
+          *reinterpret_cast<float4*>(V[a] + i0) = make_float4(v[0][a], v[1][a], v[2][a], v[3][a]);
+      }
+      *reinterpret_cast<uint4*>(K + i0) = make_uint4(kk[0], kk[1], kk[2], kk[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if (i0 + j < n) {
+          if (xchg) for (int a = 0; a < D; a++) X[a][i0 + j] = x[j][a];
+          if (vchg) for (int a = 0; a < 3; a++) V[a][i0 + j] = v[j][a];
+          K[i0 + j] = kk[j];
+        }
+      }
+    }
+    // warp-aggregated histogram of cell keys
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const unsigned m = __match_any_sync(FULL, kk[j]);
+      if (kk[j] != DEAD_KEY && lane == __ffs(m) - 1) atomicAdd(&P.cell[kk[j]], (uint32_t)__popc(m));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) removed += __shfl_xor_sync(FULL, removed, o);
+  if (lane == 0 && removed) atomicAdd(&P.ctl.counters[r * 4 + 1], (unsigned long long)removed);
+}
+
+// ================================================================ control
+__global__ void k_step_mid(Prm P) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= P.R) return;
+  const int32_t s = *P.ctl.step;
+  const int64_t n = P.ctl.n_store[r] + P.ctl.inserted[r];
+  P.ctl.n_store[r] = n;
+  P.ctl.psteps[r] += (unsigned long long)(P.ctl.live[r] + P.ctl.inserted[r]);
+  P.ctl.inserted[r] = 0;
+  const int K = P.reorder_every;
+  P.ctl.reorder[r] = ((K > 0 && (s + 1) % K == 0) || (P.cap - n < P.insert_bound)) ? 1 : 0;
+}
+
+__device__ __forceinline__ uint32_t run_lcr_base(const Prm& P, int r) {
+  return r == 0 ? 0u : P.cell[(int64_t)r * P.Nc - 1];
+}
+
+__global__ void k_step_end(Prm P, int mode, int slot) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (mode == 1) {  // explicit sample
+    if (r == 0) P.ctl.slot_done[slot] = 1;
+    return;
+  }
+  const int32_t s = *P.ctl.step;
+  if (r < P.R) {
+    const uint32_t b = run_lcr_base(P, r);
+    const uint32_t e = P.cell[(int64_t)(r + 1) * P.Nc - 1];
+    P.ctl.live[r] = (int64_t)(e - b);
+    if (P.ctl.reorder[r]) {
+      P.ctl.n_store[r] = (int64_t)(e - b);
+      P.ctl.parity[r] ^= 1;
+    }
+  }
+  if (r == 0) {
+    if ((s + 1) % P.sample_every == 0) {
+      const int sl = (s + 1) / P.sample_every - 1;
+      if (sl < P.n_slots) P.ctl.slot_done[sl] = 1;
+    }
+    *P.ctl.step = s + 1;
+  }
+}
+
+// ================================================================ Indexing
+// LCR[start[key] + rank] = global store index; warp-aggregated cursors
+__global__ void __launch_bounds__(256) k_scatter(Prm P) {
+  const int r = blockIdx.y, lane = threadIdx.x & 31;
+  const int64_t n = P.ctl.n_store[r];
+  const int64_t base = (int64_t)r * P.stride;
+  const uint32_t* K = P.key + base;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t i0w = w * 128; i0w < n; i0w += nw * 128) {
+    const int64_t i0 = i0w + lane * 4;
+    uint32_t kk[4];
+    if (i0 + 4 <= n) {
+      const uint4 q = *reinterpret_cast<const uint4*>(K + i0);
+      kk[0] = q.x; kk[1] = q.y; kk[2] = q.z; kk[3] = q.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; j++) kk[j] = i0 + j < n ? K[i0 + j] : DEAD_KEY;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const unsigned m = __match_any_sync(FULL, kk[j]);
+      const int leader = __ffs(m) - 1;
+      uint32_t p0 = 0;
+      if (kk[j] != DEAD_KEY && lane == leader) p0 = atomicAdd(&P.cell[kk[j]], (uint32_t)__popc(m));
+      p0 = __shfl_sync(FULL, p0, leader);
+      if (kk[j] != DEAD_KEY) P.lcr[p0 + __popc(m & lt)] = (uint32_t)(base + i0 + j);
+    }
+  }
+}
+
+// ============================================================= Interaction
+// Isotropic direction, Marsaglia (reading R14)
+__device__ __forceinline__ void marsaglia(uint2 key, uint32_t c, uint32_t s, uint32_t k, float e[3]) {
+  for (uint32_t blk = 0; blk < 64; blk++) {
+    const uint4 w = draw(key, c, s, TAG_COLL_DIR, k, blk);
+    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const float pp = 2.0f * u_co(ww[2 * h]) - 1.0f;
+      const float qq = 2.0f * u_co(ww[2 * h + 1]) - 1.0f;
+      const float rho = pp * pp + qq * qq;
+      if (rho < 1.0f) {
+        const float sr = sqrtf(1.0f - rho);
+        e[0] = 2.0f * pp * sr;
+        e[1] = 2.0f * qq * sr;
+        e[2] = 1.0f - 2.0f * rho;
+        return;
+      }
+    }
+  }
+  e[0] = 0.0f; e[1] = 0.0f; e[2] = 1.0f;
+}
+
+// velocity accessors: shared-memory tile, or global memory through LCR
+struct SmemCell {
+  float* vx; float* vy; float* vz; uint8_t* mod;
+  __device__ void ld(uint32_t i, float a[3]) const { a[0] = vx[i]; a[1] = vy[i]; a[2] = vz[i]; }
+  __device__ void st(uint32_t i, const float a[3]) const { vx[i] = a[0]; vy[i] = a[1]; vz[i] = a[2]; mod[i] = 1; }
+};
+struct GlobCell {
+  const uint32_t* idx; float* vx; float* vy; float* vz;
+  __device__ void ld(uint32_t i, float a[3]) const { const uint32_t g = idx[i]; a[0] = vx[g]; a[1] = vy[g]; a[2] = vz[g]; }
+  __device__ void st(uint32_t i, const float a[3]) const { const uint32_t g = idx[i]; vx[g] = a[0]; vy[g] = a[1]; vz[g] = a[2]; }
+};
+
+// NTC in one cell (readings R12-R15): M = floor(1/2 N(N-1) coef gmax + u);
+// candidate k: i = lemire(a, N), j = lemire(b, N-1) (+1 if >= i); accept iff
+// u (sigma g)_max < sigma g in fp64; g_max frozen during the step.
+template <class A>
+__device__ __forceinline__ void collide_cell(const Prm& P, uint2 key, uint32_t c, uint32_t s, uint32_t N, const A& acc,
+                                             float& gmax, uint32_t& ncand, uint32_t& nacc) {
+  ncand = 0;
+  nacc = 0;
+  if (N < 2) return;
+  const double gm = (double)gmax;
+  const double x = ((double)((int64_t)N * (int64_t)(N - 1)) * 0.5) * P.coef * gm;
+  uint4 w = draw(key, c, s, TAG_COLL_COUNT, 0, 0);
+  int64_t M = (int64_t)floor(x + u_co_d(w.x));
+  if (M > 0xFFFFFF) { latch(P, ST_CELL); M = 0xFFFFFF; }
+  double maxseen = 0.0;
+  for (uint32_t k = 0; k < (uint32_t)M; k++) {
+    w = draw(key, c, s, TAG_COLL_PAIR, k, 0);
+    const uint32_t i = lemire(w.x, N);
+    uint32_t j = lemire(w.y, N - 1);
+    if (j >= i) j++;
+    float a[3], b[3];
+    acc.ld(i, a);
+    acc.ld(j, b);
+    const float dx = a[0] - b[0], dy = a[1] - b[1], dz = a[2] - b[2];
+    const float g2 = (dx * dx + dy * dy) + dz * dz;
+    const double sg = P.model == 0 ? P.sigma_c * sqrt((double)g2) : P.sigma_c * pow((double)g2, P.omega1);
+    if (sg > maxseen) maxseen = sg;
+    if (u_co_d(w.z) * gm < sg) {
+      float e[3];
+      marsaglia(key, c, s, k, e);
+      const float cmx = (a[0] + b[0]) * 0.5f, cmy = (a[1] + b[1]) * 0.5f, cmz = (a[2] + b[2]) * 0.5f;
+      const float hh = 0.5f * sqrtf(g2);
+      const float pa[3] = {cmx + hh * e[0], cmy + hh * e[1], cmz + hh * e[2]};
+      const float pb[3] = {cmx - hh * e[0], cmy - hh * e[1], cmz - hh * e[2]};
+      acc.st(i, pa);
+      acc.st(j, pb);
+      nacc++;
+    }
+  }
+  ncand = (uint32_t)M;
+  if (maxseen > gm) gmax = (float)maxseen;
+}
+
+template <class A>
+__device__ __forceinline__ void sample_cell(const Prm& P, int slot, int64_t k, uint32_t N, const A& acc) {
+  double sx = 0.0, sy = 0.0, sz = 0.0, se = 0.0;
+  for (uint32_t i = 0; i < N; i++) {
+    float a[3];
+    acc.ld(i, a);
+    const double vx = (double)a[0], vy = (double)a[1], vz = (double)a[2];
+    sx += vx; sy += vy; sz += vz;
+    se += (vx * vx + vy * vy) + vz * vz;
+  }
+  const int64_t RN = (int64_t)P.R * P.Nc;
+  double* C = P.C + (int64_t)slot * 5 * RN + k;
+  C[0] = (double)N; C[RN] = sx; C[2 * RN] = sy; C[3 * RN] = sz; C[4 * RN] = se;
+}
+
+__device__ __forceinline__ void insertion_sort(uint32_t* a, uint32_t n) {
+  for (uint32_t i = 1; i < n; i++) {
+    const uint32_t t = a[i];
+    uint32_t j = i;
+    while (j > 0 && a[j - 1] > t) { a[j] = a[j - 1]; j--; }
+    a[j] = t;
+  }
+}
+
+__device__ void heap_sort(uint32_t* a, uint32_t n) {
+  auto sift = [&](uint32_t root, uint32_t end) {
+    while (2 * root + 1 < end) {
+      uint32_t ch = 2 * root + 1;
+      if (ch + 1 < end && a[ch] < a[ch + 1]) ch++;
+      if (a[root] < a[ch]) { const uint32_t t = a[root]; a[root] = a[ch]; a[ch] = t; root = ch; }
+      else return;
+    }
+  };
+  for (uint32_t st = n / 2; st-- > 0;) sift(st, n);
+  for (uint32_t end = n; end-- > 1;) {
+    const uint32_t t = a[0]; a[0] = a[end]; a[end] = t;
+    sift(0, end);
+  }
+}
+
+constexpr int CT = 128;    // cells per tile = threads per block
+constexpr int CAP = 2048;  // particles per tile staged in shared memory
+
+// mode 0: full step (collide, sample on sample steps, reorder); mode 1:
+// sample only into `slot` (explicit dsmc_sample)
+__global__ void __launch_bounds__(CT) k_collide(Prm P, int mode, int slot_arg) {
+  __shared__ uint32_t s_idx[CAP];
+  __shared__ float s_vx[CAP], s_vy[CAP], s_vz[CAP];
+  __shared__ uint8_t s_mod[CAP];
+  __shared__ uint32_t s_S, s_E, s_nbig, s_boff[CT], s_bn[CT];
+  const int64_t RN = (int64_t)P.R * P.Nc;
+  const int64_t k = (int64_t)blockIdx.x * CT + threadIdx.x;
+  const bool valid = k < RN;
+  const int64_t klast = ((int64_t)blockIdx.x * CT + CT - 1 < RN ? (int64_t)blockIdx.x * CT + CT - 1 : RN - 1);
+  uint32_t st = 0, en = 0;
+  if (valid) {
+    st = k == 0 ? 0u : P.cell[k - 1];
+    en = P.cell[k];
+  }
+  if (threadIdx.x == 0) { s_S = st; s_nbig = 0; }
+  if (k == klast) s_E = en;
+  const int32_t s = *P.ctl.step;
+  int slot = -1;
+  bool collide = false;
+  if (mode == 0) {
+    collide = true;
+    if ((s + 1) % P.sample_every == 0 && (s + 1) / P.sample_every - 1 < P.n_slots) slot = (s + 1) / P.sample_every - 1;
+  } else {
+    slot = slot_arg;
+  }
+  const int r = valid ? (int)(k / P.Nc) : 0;
+  const uint32_t c = valid ? (uint32_t)(k - (int64_t)r * P.Nc) : 0u;
+  const uint2 key = run_key(P, r);
+  const uint32_t N = en - st;
+  uint32_t ncand = 0, nacc = 0;
+  float gm = valid ? P.gmax[k] : 0.0f;
+  const float gm0 = gm;
+  __syncthreads();
+  const uint32_t S = s_S, E = s_E, cnt = E - S;
+  if (cnt <= (uint32_t)CAP) {
+    for (uint32_t q = threadIdx.x; q < cnt; q += CT) { s_idx[q] = P.lcr[S + q]; s_mod[q] = 0; }
+    __syncthreads();
+    const uint32_t off = st - S;
+    // canonical order (R11): small segments by their own thread, big ones by
+    // the whole block (rank sort; the values are distinct store indices)
+    if (valid && N > 1 && N <= 32) insertion_sort(s_idx + off, N);
+    if (valid && N > 32) { const uint32_t q = atomicAdd(&s_nbig, 1u); s_boff[q] = off; s_bn[q] = N; }
+    __syncthreads();
+    const uint32_t nbig = s_nbig;
+    uint32_t* s_tmp = reinterpret_cast<uint32_t*>(s_vx);
+    for (uint32_t b = 0; b < nbig; b++) {
+      const uint32_t bo = s_boff[b], bn = s_bn[b];
+      for (uint32_t q = threadIdx.x; q < bn; q += CT) {
+        const uint32_t v = s_idx[bo + q];
+        uint32_t rank = 0;
+        for (uint32_t p = 0; p < bn; p++) rank += s_idx[bo + p] < v ? 1u : 0u;
+        s_tmp[bo + rank] = v;
+      }
+      __syncthreads();
+      for (uint32_t q = threadIdx.x; q < bn; q += CT) s_idx[bo + q] = s_tmp[bo + q];
+      __syncthreads();
+    }
+    for (uint32_t q = threadIdx.x; q < cnt; q += CT) {
+      const uint32_t g = s_idx[q];
+      const int rq = (int)(g / (uint32_t)P.stride);
+      const int h = P.ctl.parity[rq];
+      s_vx[q] = parr(P, h, 3)[g];
+      s_vy[q] = parr(P, h, 4)[g];
+      s_vz[q] = parr(P, h, 5)[g];
+    }
+    __syncthreads();
+    if (valid) {
+      SmemCell A{s_vx + off, s_vy + off, s_vz + off, s_mod + off};
+      if (collide) collide_cell(P, key, c, (uint32_t)s, N, A, gm, ncand, nacc);
+      if (slot >= 0) sample_cell(P, slot, k, N, A);
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < cnt; q += CT) {
+      const uint32_t g = s_idx[q];
+      const int rq = (int)(g / (uint32_t)P.stride);
+      const int h = P.ctl.parity[rq];
+      if (mode == 0 && P.ctl.reorder[rq]) {
+        const int64_t dst = (int64_t)rq * P.stride + (int64_t)(S + q - run_lcr_base(P, rq));
+        for (int a = 0; a < P.dim; a++) parr(P, h ^ 1, a)[dst] = parr(P, h, a)[g];
+        parr(P, h ^ 1, 3)[dst] = s_vx[q];
+        parr(P, h ^ 1, 4)[dst] = s_vy[q];
+        parr(P, h ^ 1, 5)[dst] = s_vz[q];
+      } else if (s_mod[q]) {
+        parr(P, h, 3)[g] = s_vx[q];
+        parr(P, h, 4)[g] = s_vy[q];
+        parr(P, h, 5)[g] = s_vz[q];
+      }
+      if (P.debug) P.lcr[S + q] = g;
+    }
+  } else if (valid) {
+    // tile too large for shared memory: this thread works on its own cell
+    // directly in global memory (segment sorted in place in LCR)
+    uint32_t* seg = P.lcr + st;
+    if (N <= 32) insertion_sort(seg, N);
+    else heap_sort(seg, N);
+    const int h = P.ctl.parity[r];
+    GlobCell A{seg, parr(P, h, 3), parr(P, h, 4), parr(P, h, 5)};
+    if (collide) collide_cell(P, key, c, (uint32_t)s, N, A, gm, ncand, nacc);
+    if (slot >= 0) sample_cell(P, slot, k, N, A);
+    if (mode == 0 && P.ctl.reorder[r]) {
+      const uint32_t rb = run_lcr_base(P, r);
+      for (uint32_t i = 0; i < N; i++) {
+        const uint32_t g = seg[i];
+        const int64_t dst = (int64_t)r * P.stride + (int64_t)(st + i - rb);
+        for (int a = 0; a < 6; a++)
+          if (a < P.dim || a >= 3) parr(P, h ^ 1, a)[dst] = parr(P, h, a)[g];
+      }
+    }
+  }
+  if (valid && gm != gm0) P.gmax[k] = gm;
+  if (valid && P.debug && mode == 0) { P.dbg_cand[k] = ncand; P.dbg_acc[k] = (int32_t)nacc; }
+  // per-run counters: aggregate lanes of the same run
+  if (mode == 0) {
+    const uint32_t rk = valid ? (uint32_t)r : 0xFFFFFFFFu;
+    const unsigned m = __match_any_sync(FULL, rk);
+    const uint32_t sc = __reduce_add_sync(m, ncand), sa = __reduce_add_sync(m, nacc);
+    if (valid && (threadIdx.x & 31) == __ffs(m) - 1 && sc) {
+      atomicAdd(&P.ctl.counters[r * 4 + 2], (unsigned long long)sc);
+      atomicAdd(&P.ctl.counters[r * 4 + 3], (unsigned long long)sa);
+    }
+  }
+}
+
+// ============================================================== Ensemble
+// pooled ratio estimates over runs, ascending run id, + jackknife (R18)
+__device__ __forceinline__ void moments(double sn, double sx, double sy, double sz, double se, double fnum_vc,
+                                        double nr, double o[5]) {
+  o[0] = sn * fnum_vc / nr;
+  if (sn > 0) {
+    const double ux = sx / sn, uy = sy / sn, uz = sz / sn;
+    o[1] = ux; o[2] = uy; o[3] = uz;
+    o[4] = (se / sn - (ux * ux + uy * uy + uz * uz)) / 3.0;
+  } else {
+    o[1] = o[2] = o[3] = o[4] = __longlong_as_double(0x7ff8000000000000ll);
+  }
+}
+
+__global__ void k_macros(Prm P, int slot, double fnum_vc) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P.Nc) return;
+  const int64_t RN = (int64_t)P.R * P.Nc;
+  const double* C = P.C + (int64_t)slot * 5 * RN;
+  double tot[5] = {0, 0, 0, 0, 0};
+  for (int r = 0; r < P.R; r++)
+    for (int q = 0; q < 5; q++) tot[q] += C[q * RN + (int64_t)r * P.Nc + c];
+  double full[5];
+  moments(tot[0], tot[1], tot[2], tot[3], tot[4], fnum_vc, (double)P.R, full);
+  double* o = P.macros + c * 10;
+  for (int q = 0; q < 5; q++) o[q] = full[q];
+  if (P.R < 2) { for (int q = 0; q < 5; q++) o[5 + q] = 0.0; return; }
+  // two passes over runs: mean of leave-one-out estimates, then spread
+  double mean[5] = {0, 0, 0, 0, 0};
+  for (int r = 0; r < P.R; r++) {
+    double part[5], loo[5];
+    for (int q = 0; q < 5; q++) part[q] = tot[q] - C[q * RN + (int64_t)r * P.Nc + c];
+    moments(part[0], part[1], part[2], part[3], part[4], fnum_vc, (double)(P.R - 1), loo);
+    for (int q = 0; q < 5; q++) mean[q] += loo[q];
+  }
+  for (int q = 0; q < 5; q++) mean[q] /= (double)P.R;
+  double ss[5] = {0, 0, 0, 0, 0};
+  for (int r = 0; r < P.R; r++) {
+    double part[5], loo[5];
+    for (int q = 0; q < 5; q++) part[q] = tot[q] - C[q * RN + (int64_t)r * P.Nc + c];
+    moments(part[0], part[1], part[2], part[3], part[4], fnum_vc, (double)(P.R - 1), loo);
+    for (int q = 0; q < 5; q++) { const double d = loo[q] - mean[q]; ss[q] += d * d; }
+  }
+  for (int q = 0; q < 5; q++) o[5 + q] = sqrt((double)(P.R - 1) / (double)P.R * ss[q]);
+}
+
+__global__ void k_selftest_philox(int64_t n, const uint32_t* ctr, uint2 key, uint32_t* out, uint32_t* out_ref) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint4 c = make_uint4(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]);
+  const uint4 o = philox(c, key);
+  out[4 * i] = o.x; out[4 * i + 1] = o.y; out[4 * i + 2] = o.z; out[4 * i + 3] = o.w;
+  if (out_ref) {
+    const uint4 q = curand_Philox4x32_10(c, key);
+    out_ref[4 * i] = q.x; out_ref[4 * i + 1] = q.y; out_ref[4 * i + 2] = q.z; out_ref[4 * i + 3] = q.w;
+  }
+}
+
+// ============================================================ host launchers
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+static unsigned grid_cap(int64_t work, int threads, int64_t max_blocks) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return (unsigned)b;
+}
+
+void launch_zero(uint32_t* a, int64_t n, cudaStream_t st) {
+  k_zero<<<grid_cap(n / 4 + 1, 256, (int64_t)num_sms() * 8), 256, 0, st>>>(a, n);
+}
+
+void launch_fill_f32(float* a, int64_t n, float v, cudaStream_t st) {
+  k_fill_f32<<<grid_cap(n, 256, (int64_t)num_sms() * 8), 256, 0, st>>>(a, n, v);
+}
+
+int64_t scan_tiles(int64_t L) { return (L + SCAN_TILE - 1) / SCAN_TILE; }
+
+void launch_scan(uint32_t* a, int64_t L, uint32_t* part, cudaStream_t st, const LaunchHook& hook) {
+  const int64_t nb = scan_tiles(L);
+  hook.before(KSLOT_SCAN_REDUCE);
+  k_scan_reduce<<<(unsigned)nb, SCAN_T, 0, st>>>(a, L, part);
+  hook.after(KSLOT_SCAN_REDUCE);
+  hook.before(KSLOT_SCAN_PARTIALS);
+  k_scan_partials<<<1, 1024, 0, st>>>(part, nb);
+  hook.after(KSLOT_SCAN_PARTIALS);
+  hook.before(KSLOT_SCAN_DOWN);
+  k_scan_down<<<(unsigned)nb, SCAN_T, 0, st>>>(a, L, part);
+  hook.after(KSLOT_SCAN_DOWN);
+}
+
+void launch_fill(const Prm& P, cudaStream_t st) {
+  k_fill_count<<<grid_cap(P.Nc, 256, 1 << 30), 256, 0, st>>>(P);
+  launch_scan(P.cell, P.Nc, P.scan_part, st, LaunchHook{});
+  dim3 g((unsigned)((P.Nc + 7) / 8), (unsigned)P.R);
+  k_fill_emit<<<g, 256, 0, st>>>(P);
+  k_fill_finish<<<grid_cap((P.R > P.n_slots ? P.R : P.n_slots), 128, 1 << 20), 128, 0, st>>>(P);
+  launch_fill_f32(P.gmax, (int64_t)P.R * P.Nc, P.gmax0, st);
+}
+
+template <int D, bool EV>
+static void motion_t(const Prm& P, int mode, cudaStream_t st) {
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_motion<D, EV>, 256, 0);
+    if (occ < 1) occ = 1;
+  }
+  int64_t want = (int64_t)num_sms() * occ;
+  int64_t per_run = (want + P.R - 1) / P.R;
+  const int64_t need = (P.cap + 1023) / 1024;
+  if (per_run > need) per_run = need;
+  if (per_run < 1) per_run = 1;
+  dim3 g((unsigned)per_run, (unsigned)P.R);
+  k_motion<D, EV><<<g, 256, 0, st>>>(P, mode);
+}
+
+void launch_motion(const Prm& P, int mode, cudaStream_t st) {
+  const bool ev = P.has_events != 0;
+  switch (P.dim * 2 + (ev ? 1 : 0)) {
+    case 2: motion_t<1, false>(P, mode, st); break;
+    case 3: motion_t<1, true>(P, mode, st); break;
+    case 4: motion_t<2, false>(P, mode, st); break;
+    case 5: motion_t<2, true>(P, mode, st); break;
+    case 6: motion_t<3, false>(P, mode, st); break;
+    default: motion_t<3, true>(P, mode, st); break;
+  }
+}
+
+void launch_scatter(const Prm& P, cudaStream_t st) {
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter, 256, 0);
+    if (occ < 1) occ = 1;
+  }
+  int64_t want = (int64_t)num_sms() * occ;
+  int64_t per_run = (want + P.R - 1) / P.R;
+  const int64_t need = (P.cap + 1023) / 1024;
+  if (per_run > need) per_run = need;
+  if (per_run < 1) per_run = 1;
+  dim3 g((unsigned)per_run, (unsigned)P.R);
+  k_scatter<<<g, 256, 0, st>>>(P);
+}
+
+void launch_inflow(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
+  if (P.inflow_kind == 0 || P.n_face == 0) return;
+  dim3 g((unsigned)((P.n_face + 3) / 4), (unsigned)P.R);
+  hook.before(KSLOT_INFLOW_COUNT);
+  k_inflow_count<<<g, 128, 0, st>>>(P);
+  hook.after(KSLOT_INFLOW_COUNT);
+  hook.before(KSLOT_INFLOW_EMIT);
+  k_inflow_emit<<<g, 128, 0, st>>>(P);
+  hook.after(KSLOT_INFLOW_EMIT);
+}
+
+void launch_step_mid(const Prm& P, cudaStream_t st) {
+  k_step_mid<<<(P.R + 127) / 128, 128, 0, st>>>(P);
+}
+
+void launch_collide(const Prm& P, int mode, int slot, cudaStream_t st) {
+  const int64_t RN = (int64_t)P.R * P.Nc;
+  k_collide<<<(unsigned)((RN + CT - 1) / CT), CT, 0, st>>>(P, mode, slot);
+}
+
+void launch_step_end(const Prm& P, int mode, int slot, cudaStream_t st) {
+  k_step_end<<<(P.R + 127) / 128, 128, 0, st>>>(P, mode, slot);
+}
+
+void launch_macros(const Prm& P, int slot, double fnum_vc, cudaStream_t st) {
+  k_macros<<<(unsigned)((P.Nc + 127) / 128), 128, 0, st>>>(P, slot, fnum_vc);
+}
+
+void launch_selftest_philox(int64_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out,
+                            uint32_t* out_ref, cudaStream_t st) {
+  k_selftest_philox<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(n, ctr, make_uint2(k0, k1), out, out_ref);
+}
+
+// one full step: kernel order of PAPER.md Fig. 1
+void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
+  hook.before(KSLOT_ZERO);
+  launch_zero(P.cell, (int64_t)P.R * P.Nc, st);
+  hook.after(KSLOT_ZERO);
+  launch_inflow(P, st, hook);
+  hook.before(KSLOT_MOTION);
+  launch_motion(P, 0, st);
+  hook.after(KSLOT_MOTION);
+  hook.before(KSLOT_STEP_MID);
+  launch_step_mid(P, st);
+  hook.after(KSLOT_STEP_MID);
+  launch_scan(P.cell, (int64_t)P.R * P.Nc, P.scan_part, st, hook);
+  hook.before(KSLOT_SCATTER);
+  launch_scatter(P, st);
+  hook.after(KSLOT_SCATTER);
+  hook.before(KSLOT_COLLIDE);
+  launch_collide(P, 0, -1, st);
+  hook.after(KSLOT_COLLIDE);
+  hook.before(KSLOT_STEP_END);
+  launch_step_end(P, 0, 0, st);
+  hook.after(KSLOT_STEP_END);
+}
+
+void issue_sample(const Prm& P, int slot, cudaStream_t st) {
+  launch_zero(P.cell, (int64_t)P.R * P.Nc, st);
+  launch_motion(P, 1, st);
+  launch_scan(P.cell, (int64_t)P.R * P.Nc, P.scan_part, st, LaunchHook{});
+  launch_scatter(P, st);
+  launch_collide(P, 1, slot, st);
+  launch_step_end(P, 1, slot, st);
+}
+
+const char* kernel_slot_name(int k) {
+  switch (k) {
+    case KSLOT_ZERO: return "k_zero";
+    case KSLOT_INFLOW_COUNT: return "k_inflow_count";
+    case KSLOT_INFLOW_EMIT: return "k_inflow_emit";
+    case KSLOT_MOTION: return "k_motion";
+    case KSLOT_STEP_MID: return "k_step_mid";
+    case KSLOT_SCAN_REDUCE: return "k_scan_reduce";
+    case KSLOT_SCAN_PARTIALS: return "k_scan_partials";
+    case KSLOT_SCAN_DOWN: return "k_scan_down";
+    case KSLOT_SCATTER: return "k_scatter";
+    case KSLOT_COLLIDE: return "k_collide";
+    case KSLOT_STEP_END: return "k_step_end";
+    default: return "";
+  }
+}
+
+}  // namespace dsmc

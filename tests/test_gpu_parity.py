@@ -1,0 +1,258 @@
+"""GPU path vs oracle (north-star criteria (1)-(3)), through the C ABI.
+
+(1) from identical state, one step: cell keys/LCR/per-cell counts, NTC
+    candidate and accepted-pair counts are bit-exact;
+(2) positions and velocities agree within 1e-5 relative (we observe bit-exact);
+(3) ensemble density/velocity/temperature agree within max(3 SE, 1%).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from workloads import configs, inputs
+
+pytestmark = pytest.mark.gpu
+
+STATE_KEYS = ("x", "y", "z", "vx", "vy", "vz")
+
+
+def close_rel(a, b, scale):
+    return np.abs(a.astype(np.float64) - b.astype(np.float64)) <= 1e-5 * np.maximum(np.abs(b), scale)
+
+
+def compare_state(got, want, p, tag=""):
+    assert len(got["x"]) == len(want["x"]), (tag, len(got["x"]), len(want["x"]))
+    al = want["alive"] == 1
+    assert np.array_equal(got["alive"], want["alive"]), tag
+    D = p["dim"]
+    n_exact = 0
+    for k in STATE_KEYS:
+        if k in ("y", "z") and "xyz".index(k) >= D:
+            continue
+        g, w = got[k][al], want[k][al]
+        scale = 1.0 if k in "xyz" else math.sqrt(p.get("T_ref", 1.0))
+        ok = close_rel(g, w, scale)
+        assert ok.all(), (tag, k, np.nonzero(~ok)[0][:5], g[~ok][:5], w[~ok][:5])
+        n_exact += int((g == w).sum())
+    return n_exact
+
+
+def one_step_case(dsmc_gpu, oracle_mod, p, run, s0, seed_state=None):
+    """Oracle runs `run` to step s0 (or takes a seeded random state), the GPU
+    batch is given that exact state, both advance one step, compare."""
+    sim = dsmc_gpu.Simulation(p, debug=True)
+    sim.generate()
+    ref = oracle_mod.OracleRun(p, run)
+    if seed_state is None:
+        ref.fill()
+        ref.step(s0)
+    else:
+        ref.set_state(seed_state, step=s0)
+    st = ref.get_state()
+    sim.set_state(run - p["run_id0"], st, step=s0)
+    sim.set_gmax(run - p["run_id0"], ref.get_gmax())
+    sim.step(1)
+    ref.step(1)
+    rc, counters = sim.status()
+    assert rc == 0 and ref.status == 0
+    r = run - p["run_id0"]
+    got, want = sim.get_state(r), ref.get_state()
+    compare_state(got, want, p, tag=f"run {run} step {s0}")
+    gi, oi = sim.get_index(r), ref.get_index()
+    assert np.array_equal(gi["count"], oi["count"])
+    assert np.array_equal(gi["start"], oi["start"])
+    assert np.array_equal(gi["lcr"], oi["lcr"])
+    cand, acc = ref.get_cell_stats()
+    assert np.array_equal(gi["cand"], cand)
+    assert np.array_equal(gi["acc"], acc)
+    assert np.array_equal(sim.get_gmax(r), ref.get_gmax())
+    oc = ref.counters()
+    return sim, ref, counters[r], oc
+
+
+def test_philox_matches_curand_and_oracle(dsmc_gpu, oracle_mod):
+    rng = np.random.Generator(np.random.PCG64(3))
+    ctr = rng.integers(0, 2 ** 32, size=(4096, 4), dtype=np.uint64).astype(np.uint32)
+    out, ref = dsmc_gpu.dsmc_selftest_philox(ctr, 0x12345678, 0x9ABCDEF0)
+    assert np.array_equal(out, ref)
+    for i in range(0, 4096, 97):
+        assert np.array_equal(out[i], oracle_mod.philox(ctr[i], [0x12345678, 0x9ABCDEF0]))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2_small", "c3_small", "c4_small", "c5_small"])
+def test_fill_matches_oracle(dsmc_gpu, oracle_mod, name):
+    p = configs.get(name)
+    sim = dsmc_gpu.Simulation(p)
+    sim.generate()
+    for r in sorted({0, p["n_runs"] - 1}):
+        ref = oracle_mod.OracleRun(p, r)
+        ref.fill()
+        want = ref.get_state()
+        got = sim.get_state(r)
+        for k in ("x", "y", "z"):
+            assert np.array_equal(got[k], want[k]), k     # no transcendental on positions
+        compare_state(got, want, p)
+        assert np.array_equal(sim.get_gmax(r), ref.get_gmax())
+
+
+@pytest.mark.parametrize("name,s0", [("c1", 0), ("c1", 3), ("c1", 57), ("c4_small", 0), ("c4_small", 3),
+                                     ("c2_small", 0), ("c2_small", 7), ("c3_small", 0), ("c3_small", 11),
+                                     ("c5_small", 0), ("c5_small", 15)])
+def test_one_step_parity(dsmc_gpu, oracle_mod, name, s0):
+    """Criteria (1)+(2) at steps {0, reorder step (s0+1 = 4k), others}."""
+    p = configs.get(name)
+    for run in sorted({0, p["n_runs"] - 1}):
+        one_step_case(dsmc_gpu, oracle_mod, p, run, s0)
+
+
+def test_one_step_parity_random_state_with_dead(dsmc_gpu, oracle_mod):
+    """Arbitrary seeded state with removed-but-not-compacted slots."""
+    p = configs.get("c4_small")
+    p["reorder_every"] = 0
+    st = inputs.random_state(12, p, 30_000, dead_frac=0.05)
+    one_step_case(dsmc_gpu, oracle_mod, p, 1, 5, seed_state=st)
+
+
+def test_one_step_parity_heavy_cells(dsmc_gpu, oracle_mod):
+    """Occupancy skew (SURVEY hard parts): cells with hundreds to thousands of
+    particles exercise the block rank-sort and the global-memory tile path."""
+    p = configs.get("c4_small")
+    p["reorder_every"] = 1
+    cells = [5, 6, 7, 300, 301, 2000]
+    st = inputs.clustered_state(4, p, cells, 700)
+    st2 = inputs.clustered_state(5, p, [9], 3000)
+    for k in st:
+        st[k] = np.concatenate([st[k], st2[k]])
+    p["cap_per_run"] = len(st["x"]) + 64
+    one_step_case(dsmc_gpu, oracle_mod, p, 0, 2, seed_state=st)
+
+
+def test_run_independent_of_batch(dsmc_gpu):
+    """S:288 'strategies change time, never answers': run r computed alone
+    (n=1, run_id0=r) equals run r inside a batch, bit for bit."""
+    p = configs.get("c2_small", n_runs=4, n_steps=20)
+    big = dsmc_gpu.Simulation(p)
+    big.generate()
+    big.step(20)
+    q = dict(p)
+    q["n_runs"] = 1
+    q["run_id0"] = 2
+    one = dsmc_gpu.Simulation(q)
+    one.generate()
+    one.step(20)
+    a, b = big.get_state(2), one.get_state(0)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+
+
+def ensemble_compare(gpu_macros, ora_macros, min_count_rho=None):
+    """Criterion (3): |gpu - oracle| <= max(3 sqrt(SE_g^2 + SE_o^2), 1% |oracle|)."""
+    bad = 0
+    tot = 0
+    for q in range(5):
+        g, o = gpu_macros[:, q], ora_macros[:, q]
+        se = np.sqrt(gpu_macros[:, 5 + q] ** 2 + ora_macros[:, 5 + q] ** 2)
+        m = np.isfinite(g) & np.isfinite(o)
+        tol = np.maximum(3 * se, 0.01 * np.abs(o))
+        bad += int((np.abs(g - o)[m] > tol[m]).sum())
+        tot += int(m.sum())
+    return bad, tot
+
+
+@pytest.mark.parametrize("name", ["c1", "c2_small", "c3_small", "c5_small"])
+def test_ensemble_parity(dsmc_gpu, oracle_mod, name):
+    """Criterion (3) on full runs (reduced sizes for c2/c3/c5)."""
+    p = configs.get(name)
+    nst = configs.n_steps(p)
+    sim = dsmc_gpu.Simulation(p)
+    sim.generate()
+    sim.step(nst)
+    rc, _ = sim.status()
+    assert rc == 0
+    runs = [oracle_mod.OracleRun(p, r) for r in range(p["n_runs"])]
+    for o in runs:
+        o.fill()
+        o.step(nst)
+    total_bad = total = 0
+    exact = 0
+    for slot in range(configs.n_slots(p)):
+        gm = sim.read_macros(slot)
+        sums = np.array([o.get_snap(slot) for o in runs])
+        om = oracle_mod.ensemble(sums, p["fnum_vc"])
+        b, t = ensemble_compare(gm, om)
+        total_bad += b
+        total += t
+        exact += int(np.array_equal(sim.read_sums(slot), sums.transpose(1, 0, 2)))
+    assert total_bad <= max(1, 0.01 * total), (total_bad, total)
+    print(f"{name}: {total_bad}/{total} entries outside tolerance; bit-identical slots {exact}")
+
+
+def test_hs_rate_gpu(dsmc_gpu):
+    """GPU equilibrium box: accepted collisions = n^2 sigma <g>/2 V dt / F_N within 1%."""
+    p = configs.get("c4", n_runs=4, n_steps=20)
+    sim = dsmc_gpu.Simulation(p)
+    sim.generate()
+    sim.step(5)
+    _, c0 = sim.status()
+    sim.step(15)
+    _, c1 = sim.status()
+    acc = sum(b["accepted"] - a["accepted"] for a, b in zip(c0, c1))
+    Nc = 64 ** 3
+    n_d = 10 * p["fnum_vc"]
+    expect = 0.5 * n_d * n_d * math.pi * (4 / math.sqrt(math.pi)) * Nc * p["dt"] / p["fnum_vc"] * 15 * 4
+    assert abs(acc / expect - 1) < 0.01, acc / expect
+    for b in c1:
+        assert b["n_store"] == Nc * 10
+
+
+def test_full_size_c4_sampled_parity(dsmc_gpu, oracle_mod):
+    """BASELINE size (64^3, 10 ppc) in the bench's launch configuration: one
+    run of a 16-run batch after 7 steps is handed to the oracle; one more step
+    must match (criteria (1)+(2) on the full-size state)."""
+    p = configs.get("c4", n_runs=16, n_steps=100)
+    sim = dsmc_gpu.Simulation(p, debug=True)
+    sim.generate()
+    sim.step(7)
+    r = 13
+    st = sim.get_state(r)
+    ref = oracle_mod.OracleRun(p, r)
+    ref.set_state(st, step=7)
+    ref.set_gmax(sim.get_gmax(r))
+    sim.step(1)
+    ref.step(1)
+    compare_state(sim.get_state(r), ref.get_state(), p)
+    gi, oi = sim.get_index(r), ref.get_index()
+    assert np.array_equal(gi["lcr"], oi["lcr"])
+    cand, acc = ref.get_cell_stats()
+    assert np.array_equal(gi["cand"], cand) and np.array_equal(gi["acc"], acc)
+
+
+def test_open_count_balance_gpu(dsmc_gpu):
+    for name in ("c2_small", "c3_small", "c5_small"):
+        p = configs.get(name)
+        sim = dsmc_gpu.Simulation(p)
+        sim.generate()
+        n0 = [int(sim.get_state(r)["alive"].sum()) for r in range(p["n_runs"])]
+        sim.step(20)
+        rc, c = sim.status()
+        assert rc == 0
+        for r in range(p["n_runs"]):
+            live = int(sim.get_state(r)["alive"].sum())
+            assert live == n0[r] + c[r]["inserted"] - c[r]["removed"], name
+
+
+def test_explicit_sample_matches_oracle(dsmc_gpu, oracle_mod):
+    p = configs.get("c2_small", n_steps=20)
+    sim = dsmc_gpu.Simulation(p)
+    sim.generate()
+    sim.step(5)
+    sim.sample(0)
+    ref = [oracle_mod.OracleRun(p, r) for r in range(p["n_runs"])]
+    for o in ref:
+        o.fill()
+        o.step(5)
+        o.sample(0)
+    sums = np.array([o.get_snap(0) for o in ref])
+    g = sim.read_sums(0)
+    assert np.allclose(g, sums.transpose(1, 0, 2), rtol=1e-6, atol=1e-5)
