@@ -517,8 +517,11 @@ int dsmc_get_state(dsmc_ctx* c, int32_t run, int64_t* n_out, float* x, float* y,
   if (rc) return rc;
   *n_out = n;
   float* dst[6] = {x, y, z, vx, vy, vz};
-  for (int a = 0; a < 6; a++)
-    if (dst[a] && n) CK(cudaMemcpyAsync(dst[a], arr(c, h, a, run), 4 * (size_t)n, cudaMemcpyDeviceToHost, c->stream));
+  for (int a = 0; a < 6; a++) {
+    if (!dst[a] || !n) continue;
+    if (a < 3 && a >= c->prob.dim) std::memset(dst[a], 0, 4 * (size_t)n);  // axes >= dim are 0
+    else CK(cudaMemcpyAsync(dst[a], arr(c, h, a, run), 4 * (size_t)n, cudaMemcpyDeviceToHost, c->stream));
+  }
   CK(cudaStreamSynchronize(c->stream));
   if (alive) {
     std::vector<float> tmp;

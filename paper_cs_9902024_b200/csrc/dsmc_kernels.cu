@@ -435,7 +435,10 @@ __device__ __forceinline__ uint32_t enumerate(const Prm& P, const float x[3], co
   return kbase + (uint32_t)(ic[0] + P.nx * (ic[1] + P.ny * ic[2]));
 }
 
-// persistent over (run = blockIdx.y, 4 consecutive particles per lane);
+// persistent over (run = blockIdx.y, warp chunks of 128 particles; lane owns
+// particles chunk + 32 j + lane, j < 4, so that the 32 keys of one warp
+// instruction are consecutive store slots -- after a reorder they share few
+// cells and the warp-aggregated histogram needs few atomics).
 // mode 0: move + enumerate, mode 1: enumerate only (explicit Sampling)
 template <int D, bool EV>
 __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
@@ -455,71 +458,45 @@ __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
   const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   uint32_t removed = 0;
   for (int64_t i0w = w * 128; i0w < n; i0w += nw * 128) {
-    const int64_t i0 = i0w + lane * 4;
     float x[4][3], v[4][3];
-    const bool full = i0 + 4 <= n;
-    if (full) {
-#pragma unroll
-      for (int a = 0; a < D; a++) {
-        const float4 q = *reinterpret_cast<const float4*>(X[a] + i0);
-        x[0][a] = q.x; x[1][a] = q.y; x[2][a] = q.z; x[3][a] = q.w;
-      }
-#pragma unroll
-      for (int a = 0; a < 3; a++) {
-        const float4 q = *reinterpret_cast<const float4*>(V[a] + i0);
-        v[0][a] = q.x; v[1][a] = q.y; v[2][a] = q.z; v[3][a] = q.w;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const bool in = i0 + j < n;
-#pragma unroll
-        for (int a = 0; a < D; a++) x[j][a] = in ? X[a][i0 + j] : DEAD_X;
-#pragma unroll
-        for (int a = 0; a < 3; a++) v[j][a] = in ? V[a][i0 + j] : 0.0f;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; j++)
-#pragma unroll
-      for (int a = D; a < 3; a++) x[j][a] = 0.0f;
-    uint32_t kk[4];
-    bool vchg = false, xchg = false;
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      if (x[j][0] < -1.0e29f) { kk[j] = DEAD_KEY; continue; }
-      if (mode == 0) {
-        xchg = true;
-        if (move_one<D, EV>(P, key, (uint32_t)(i0 + j), s, x[j], v[j], vchg)) {
-          x[j][0] = DEAD_X;
-          kk[j] = DEAD_KEY;
-          removed++;
-          continue;
-        }
-      }
-      kk[j] = enumerate<D>(P, x[j], v[j], kbase);
+      const int64_t i = i0w + j * 32 + lane;
+      const bool in = i < n;
+#pragma unroll
+      for (int a = 0; a < D; a++) x[j][a] = in ? X[a][i] : DEAD_X;
+#pragma unroll
+      for (int a = D; a < 3; a++) x[j][a] = 0.0f;
+#pragma unroll
+      for (int a = 0; a < 3; a++) v[j][a] = in ? V[a][i] : 0.0f;
     }
-    if (full) {
-      if (xchg) {
+    uint32_t kk[4];
 #pragma unroll
-        for (int a = 0; a < D; a++)
-          *reinterpret_cast<float4*>(X[a] + i0) = make_float4(x[0][a], x[1][a], x[2][a], x[3][a]);
-      }
-      if (vchg) {
+    for (int j = 0; j < 4; j++) {
+      const int64_t i = i0w + j * 32 + lane;
+      bool vchg = false;
+      if (x[j][0] < -1.0e29f) {
+        kk[j] = DEAD_KEY;
+      } else {
+        bool dead = false;
+        if (mode == 0) {
+          dead = move_one<D, EV>(P, key, (uint32_t)i, s, x[j], v[j], vchg);
+          if (dead) { x[j][0] = DEAD_X; removed++; }
+        }
+        kk[j] = dead ? DEAD_KEY : enumerate<D>(P, x[j], v[j], kbase);
+        if (mode == 0) {
+          X[0][i] = x[j][0];
+          if (!dead) {
 #pragma unroll
-        for (int a = 0; a < 3; a++)
-          *reinterpret_cast<float4*>(V[a] + i0) = make_float4(v[0][a], v[1][a], v[2][a], v[3][a]);
-      }
-      *reinterpret_cast<uint4*>(K + i0) = make_uint4(kk[0], kk[1], kk[2], kk[3]);
-    } else {
+            for (int a = 1; a < D; a++) X[a][i] = x[j][a];
+            if (vchg) {
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        if (i0 + j < n) {
-          if (xchg) for (int a = 0; a < D; a++) X[a][i0 + j] = x[j][a];
-          if (vchg) for (int a = 0; a < 3; a++) V[a][i0 + j] = v[j][a];
-          K[i0 + j] = kk[j];
+              for (int a = 0; a < 3; a++) V[a][i] = v[j][a];
+            }
+          }
         }
       }
+      if (i < n) K[i] = kk[j];
     }
     // warp-aggregated histogram of cell keys
 #pragma unroll
@@ -576,7 +553,9 @@ __global__ void k_step_end(Prm P, int mode, int slot) {
 }
 
 // ================================================================ Indexing
-// LCR[start[key] + rank] = global store index; warp-aggregated cursors
+// LCR[start[key] + rank] = global store index; warp-aggregated cursors over
+// lane-contiguous particles (same chunking as k_motion); the four atomics of
+// a chunk are issued before any result is consumed.
 __global__ void __launch_bounds__(256) k_scatter(Prm P) {
   const int r = blockIdx.y, lane = threadIdx.x & 31;
   const int64_t n = P.ctl.n_store[r];
@@ -586,23 +565,23 @@ __global__ void __launch_bounds__(256) k_scatter(Prm P) {
   const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const unsigned lt = (1u << lane) - 1u;
   for (int64_t i0w = w * 128; i0w < n; i0w += nw * 128) {
-    const int64_t i0 = i0w + lane * 4;
-    uint32_t kk[4];
-    if (i0 + 4 <= n) {
-      const uint4 q = *reinterpret_cast<const uint4*>(K + i0);
-      kk[0] = q.x; kk[1] = q.y; kk[2] = q.z; kk[3] = q.w;
-    } else {
+    uint32_t kk[4], m[4], p0[4];
 #pragma unroll
-      for (int j = 0; j < 4; j++) kk[j] = i0 + j < n ? K[i0 + j] : DEAD_KEY;
+    for (int j = 0; j < 4; j++) {
+      const int64_t i = i0w + j * 32 + lane;
+      kk[j] = i < n ? K[i] : DEAD_KEY;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) m[j] = __match_any_sync(FULL, kk[j]);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      p0[j] = 0;
+      if (kk[j] != DEAD_KEY && lane == __ffs(m[j]) - 1) p0[j] = atomicAdd(&P.cell[kk[j]], (uint32_t)__popc(m[j]));
     }
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      const unsigned m = __match_any_sync(FULL, kk[j]);
-      const int leader = __ffs(m) - 1;
-      uint32_t p0 = 0;
-      if (kk[j] != DEAD_KEY && lane == leader) p0 = atomicAdd(&P.cell[kk[j]], (uint32_t)__popc(m));
-      p0 = __shfl_sync(FULL, p0, leader);
-      if (kk[j] != DEAD_KEY) P.lcr[p0 + __popc(m & lt)] = (uint32_t)(base + i0 + j);
+      const uint32_t b = __shfl_sync(FULL, p0[j], __ffs(m[j]) - 1);
+      if (kk[j] != DEAD_KEY) P.lcr[b + __popc(m[j] & lt)] = (uint32_t)(base + i0w + j * 32 + lane);
     }
   }
 }
@@ -725,90 +704,119 @@ __device__ void heap_sort(uint32_t* a, uint32_t n) {
   }
 }
 
-constexpr int CT = 128;    // cells per tile = threads per block
-constexpr int CAP = 2048;  // particles per tile staged in shared memory
+constexpr int CT = 128;     // cells per tile = threads per block
+constexpr int CAP = 1536;   // particles per tile staged in shared memory
 
+// One block = a tile of CT consecutive (run, cell) keys; thread t owns cell t.
 // mode 0: full step (collide, sample on sample steps, reorder); mode 1:
-// sample only into `slot` (explicit dsmc_sample)
-__global__ void __launch_bounds__(CT) k_collide(Prm P, int mode, int slot_arg) {
-  __shared__ uint32_t s_idx[CAP];
-  __shared__ float s_vx[CAP], s_vy[CAP], s_vz[CAP];
-  __shared__ uint8_t s_mod[CAP];
-  __shared__ uint32_t s_S, s_E, s_nbig, s_boff[CT], s_bn[CT];
+// sample only into `slot` (explicit dsmc_sample).
+//   A  segment bounds, per-run metadata (parity, reorder flag, LCR base)
+//   B  stage the tile's LCR slice; tag each position with its cell
+//   C  canonical order (R11): rank of each element inside its segment
+//   D  gather velocities in canonical order; reorder: copy positions
+//   E  NTC per cell (thread per cell) + Sampling
+//   F  write modified velocities back (or the whole tile, reordered)
+template <int D>
+__global__ void __launch_bounds__(CT, 7) k_collide(Prm P, int mode, int slot_arg) {
+  __shared__ uint32_t s_sorted[CAP];
+  __shared__ uint32_t s_a[CAP];       // raw LCR slice, then vx bits
+  __shared__ float s_vy[CAP], s_vz[CAP];
+  __shared__ uint8_t s_cell[CAP], s_mod[CAP];
+  __shared__ uint32_t s_st[CT], s_n[CT], s_base[CT];
+  __shared__ uint8_t s_ro[CT], s_h[CT], s_reo[CT];
+  __shared__ uint32_t s_S, s_E;
+  const int t = threadIdx.x;
   const int64_t RN = (int64_t)P.R * P.Nc;
-  const int64_t k = (int64_t)blockIdx.x * CT + threadIdx.x;
+  const int64_t k0 = (int64_t)blockIdx.x * CT;
+  const int64_t k = k0 + t;
   const bool valid = k < RN;
-  const int64_t klast = ((int64_t)blockIdx.x * CT + CT - 1 < RN ? (int64_t)blockIdx.x * CT + CT - 1 : RN - 1);
+  const int64_t klast = (k0 + CT - 1 < RN ? k0 + CT - 1 : RN - 1);
+  const int r_first = (int)(k0 / P.Nc);
+  const int nr = (int)(klast / P.Nc) - r_first + 1;
   uint32_t st = 0, en = 0;
   if (valid) {
     st = k == 0 ? 0u : P.cell[k - 1];
     en = P.cell[k];
   }
-  if (threadIdx.x == 0) { s_S = st; s_nbig = 0; }
+  const int r = valid ? (int)(k / P.Nc) : r_first;
+  const uint32_t c = valid ? (uint32_t)(k - (int64_t)r * P.Nc) : 0u;
+  const uint32_t N = en - st;
+  if (t == 0) s_S = st;
   if (k == klast) s_E = en;
+  s_st[t] = st;
+  s_n[t] = N;
+  s_ro[t] = (uint8_t)(r - r_first);
+  if (t < nr) {
+    const int rr = r_first + t;
+    s_h[t] = (uint8_t)P.ctl.parity[rr];
+    s_reo[t] = (uint8_t)(mode == 0 ? P.ctl.reorder[rr] : 0);
+    s_base[t] = run_lcr_base(P, rr);
+  }
   const int32_t s = *P.ctl.step;
   int slot = -1;
-  bool collide = false;
+  const bool collide = mode == 0;
   if (mode == 0) {
-    collide = true;
     if ((s + 1) % P.sample_every == 0 && (s + 1) / P.sample_every - 1 < P.n_slots) slot = (s + 1) / P.sample_every - 1;
   } else {
     slot = slot_arg;
   }
-  const int r = valid ? (int)(k / P.Nc) : 0;
-  const uint32_t c = valid ? (uint32_t)(k - (int64_t)r * P.Nc) : 0u;
   const uint2 key = run_key(P, r);
-  const uint32_t N = en - st;
   uint32_t ncand = 0, nacc = 0;
   float gm = valid ? P.gmax[k] : 0.0f;
   const float gm0 = gm;
   __syncthreads();
   const uint32_t S = s_S, E = s_E, cnt = E - S;
   if (cnt <= (uint32_t)CAP) {
-    for (uint32_t q = threadIdx.x; q < cnt; q += CT) { s_idx[q] = P.lcr[S + q]; s_mod[q] = 0; }
-    __syncthreads();
     const uint32_t off = st - S;
-    // canonical order (R11): small segments by their own thread, big ones by
-    // the whole block (rank sort; the values are distinct store indices)
-    if (valid && N > 1 && N <= 32) insertion_sort(s_idx + off, N);
-    if (valid && N > 32) { const uint32_t q = atomicAdd(&s_nbig, 1u); s_boff[q] = off; s_bn[q] = N; }
+    // B
+    for (uint32_t q = t; q < cnt; q += CT) s_a[q] = P.lcr[S + q];
+    if (valid) for (uint32_t i = 0; i < N; i++) s_cell[off + i] = (uint8_t)t;
     __syncthreads();
-    const uint32_t nbig = s_nbig;
-    uint32_t* s_tmp = reinterpret_cast<uint32_t*>(s_vx);
-    for (uint32_t b = 0; b < nbig; b++) {
-      const uint32_t bo = s_boff[b], bn = s_bn[b];
-      for (uint32_t q = threadIdx.x; q < bn; q += CT) {
-        const uint32_t v = s_idx[bo + q];
-        uint32_t rank = 0;
-        for (uint32_t p = 0; p < bn; p++) rank += s_idx[bo + p] < v ? 1u : 0u;
-        s_tmp[bo + rank] = v;
+    // C: values are distinct store indices -> rank = #smaller in the segment
+    for (uint32_t q = t; q < cnt; q += CT) {
+      const int cq = s_cell[q];
+      const uint32_t b = s_st[cq] - S, n = s_n[cq];
+      const uint32_t v = s_a[q];
+      uint32_t rank = 0;
+      for (uint32_t p = 0; p < n; p++) rank += s_a[b + p] < v ? 1u : 0u;
+      s_sorted[b + rank] = v;
+    }
+    __syncthreads();
+    // D
+    float* s_vx = reinterpret_cast<float*>(s_a);
+    for (uint32_t q = t; q < cnt; q += CT) {
+      const uint32_t g = s_sorted[q];
+      const int ro = s_ro[s_cell[q]];
+      const int h = s_h[ro];
+      const float vx = parr(P, h, 3)[g], vy = parr(P, h, 4)[g], vz = parr(P, h, 5)[g];
+      if (s_reo[ro]) {
+        const int64_t dst = (int64_t)(r_first + ro) * P.stride + (int64_t)(S + q - s_base[ro]);
+        float xs[D];
+#pragma unroll
+        for (int a = 0; a < D; a++) xs[a] = parr(P, h, a)[g];
+#pragma unroll
+        for (int a = 0; a < D; a++) parr(P, h ^ 1, a)[dst] = xs[a];
       }
-      __syncthreads();
-      for (uint32_t q = threadIdx.x; q < bn; q += CT) s_idx[bo + q] = s_tmp[bo + q];
-      __syncthreads();
-    }
-    for (uint32_t q = threadIdx.x; q < cnt; q += CT) {
-      const uint32_t g = s_idx[q];
-      const int rq = (int)(g / (uint32_t)P.stride);
-      const int h = P.ctl.parity[rq];
-      s_vx[q] = parr(P, h, 3)[g];
-      s_vy[q] = parr(P, h, 4)[g];
-      s_vz[q] = parr(P, h, 5)[g];
+      s_vx[q] = vx;
+      s_vy[q] = vy;
+      s_vz[q] = vz;
+      s_mod[q] = 0;
     }
     __syncthreads();
+    // E
     if (valid) {
       SmemCell A{s_vx + off, s_vy + off, s_vz + off, s_mod + off};
       if (collide) collide_cell(P, key, c, (uint32_t)s, N, A, gm, ncand, nacc);
       if (slot >= 0) sample_cell(P, slot, k, N, A);
     }
     __syncthreads();
-    for (uint32_t q = threadIdx.x; q < cnt; q += CT) {
-      const uint32_t g = s_idx[q];
-      const int rq = (int)(g / (uint32_t)P.stride);
-      const int h = P.ctl.parity[rq];
-      if (mode == 0 && P.ctl.reorder[rq]) {
-        const int64_t dst = (int64_t)rq * P.stride + (int64_t)(S + q - run_lcr_base(P, rq));
-        for (int a = 0; a < P.dim; a++) parr(P, h ^ 1, a)[dst] = parr(P, h, a)[g];
+    // F
+    for (uint32_t q = t; q < cnt; q += CT) {
+      const uint32_t g = s_sorted[q];
+      const int ro = s_ro[s_cell[q]];
+      const int h = s_h[ro];
+      if (s_reo[ro]) {
+        const int64_t dst = (int64_t)(r_first + ro) * P.stride + (int64_t)(S + q - s_base[ro]);
         parr(P, h ^ 1, 3)[dst] = s_vx[q];
         parr(P, h ^ 1, 4)[dst] = s_vy[q];
         parr(P, h ^ 1, 5)[dst] = s_vz[q];
@@ -825,17 +833,20 @@ __global__ void __launch_bounds__(CT) k_collide(Prm P, int mode, int slot_arg) {
     uint32_t* seg = P.lcr + st;
     if (N <= 32) insertion_sort(seg, N);
     else heap_sort(seg, N);
-    const int h = P.ctl.parity[r];
+    const int ro = r - r_first;
+    const int h = s_h[ro];
     GlobCell A{seg, parr(P, h, 3), parr(P, h, 4), parr(P, h, 5)};
     if (collide) collide_cell(P, key, c, (uint32_t)s, N, A, gm, ncand, nacc);
     if (slot >= 0) sample_cell(P, slot, k, N, A);
-    if (mode == 0 && P.ctl.reorder[r]) {
-      const uint32_t rb = run_lcr_base(P, r);
+    if (s_reo[ro]) {
+      const uint32_t rb = s_base[ro];
       for (uint32_t i = 0; i < N; i++) {
         const uint32_t g = seg[i];
         const int64_t dst = (int64_t)r * P.stride + (int64_t)(st + i - rb);
-        for (int a = 0; a < 6; a++)
-          if (a < P.dim || a >= 3) parr(P, h ^ 1, a)[dst] = parr(P, h, a)[g];
+#pragma unroll
+        for (int a = 0; a < D; a++) parr(P, h ^ 1, a)[dst] = parr(P, h, a)[g];
+#pragma unroll
+        for (int a = 3; a < 6; a++) parr(P, h ^ 1, a)[dst] = parr(P, h, a)[g];
       }
     }
   }
@@ -846,7 +857,7 @@ __global__ void __launch_bounds__(CT) k_collide(Prm P, int mode, int slot_arg) {
     const uint32_t rk = valid ? (uint32_t)r : 0xFFFFFFFFu;
     const unsigned m = __match_any_sync(FULL, rk);
     const uint32_t sc = __reduce_add_sync(m, ncand), sa = __reduce_add_sync(m, nacc);
-    if (valid && (threadIdx.x & 31) == __ffs(m) - 1 && sc) {
+    if (valid && (t & 31) == __ffs(m) - 1 && sc) {
       atomicAdd(&P.ctl.counters[r * 4 + 2], (unsigned long long)sc);
       atomicAdd(&P.ctl.counters[r * 4 + 3], (unsigned long long)sa);
     }
@@ -1022,7 +1033,10 @@ void launch_step_mid(const Prm& P, cudaStream_t st) {
 
 void launch_collide(const Prm& P, int mode, int slot, cudaStream_t st) {
   const int64_t RN = (int64_t)P.R * P.Nc;
-  k_collide<<<(unsigned)((RN + CT - 1) / CT), CT, 0, st>>>(P, mode, slot);
+  const unsigned g = (unsigned)((RN + CT - 1) / CT);
+  if (P.dim == 1) k_collide<1><<<g, CT, 0, st>>>(P, mode, slot);
+  else if (P.dim == 2) k_collide<2><<<g, CT, 0, st>>>(P, mode, slot);
+  else k_collide<3><<<g, CT, 0, st>>>(P, mode, slot);
 }
 
 void launch_step_end(const Prm& P, int mode, int slot, cudaStream_t st) {

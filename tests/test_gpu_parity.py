@@ -119,6 +119,7 @@ def test_one_step_parity_heavy_cells(dsmc_gpu, oracle_mod):
     particles exercise the block rank-sort and the global-memory tile path."""
     p = configs.get("c4_small")
     p["reorder_every"] = 1
+    p["fill"] = []                      # generate() must not overflow the small capacity
     cells = [5, 6, 7, 300, 301, 2000]
     st = inputs.clustered_state(4, p, cells, 700)
     st2 = inputs.clustered_state(5, p, [9], 3000)
