@@ -442,8 +442,15 @@ __device__ __forceinline__ uint32_t enumerate(const Prm& P, const float x[3], co
 // mode 0: move + enumerate, mode 1: enumerate only (explicit Sampling)
 template <int D, bool EV>
 __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
-  const int r = blockIdx.y, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
+  const uint32_t s = (uint32_t)*P.ctl.step;
+  const int64_t items_per_run = (P.cap + 1023) / 1024;
+  const int64_t n_items = items_per_run * P.R;
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+  const int r = (int)(item / items_per_run);
   const int64_t n = P.ctl.n_store[r];
+  const int64_t i0w = (item - (int64_t)r * items_per_run) * 1024 + (threadIdx.x >> 5) * 128;
+  if (i0w - (threadIdx.x >> 5) * 128 >= n) continue;
   const int h = P.ctl.parity[r];
   const int64_t base = (int64_t)r * P.stride;
   float* X[3];
@@ -452,12 +459,9 @@ __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
   for (int a = 0; a < 3; a++) { X[a] = parr(P, h, a) + base; V[a] = parr(P, h, 3 + a) + base; }
   uint32_t* K = P.key + base;
   const uint2 key = run_key(P, r);
-  const uint32_t s = (uint32_t)*P.ctl.step;
   const uint32_t kbase = (uint32_t)r * (uint32_t)P.Nc;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   uint32_t removed = 0;
-  for (int64_t i0w = w * 128; i0w < n; i0w += nw * 128) {
+  {
     float x[4][3], v[4][3];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
@@ -508,6 +512,7 @@ __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) removed += __shfl_xor_sync(FULL, removed, o);
   if (lane == 0 && removed) atomicAdd(&P.ctl.counters[r * 4 + 1], (unsigned long long)removed);
+  }
 }
 
 // ================================================================ control
@@ -557,14 +562,17 @@ __global__ void k_step_end(Prm P, int mode, int slot) {
 // lane-contiguous particles (same chunking as k_motion); the four atomics of
 // a chunk are issued before any result is consumed.
 __global__ void __launch_bounds__(256) k_scatter(Prm P) {
-  const int r = blockIdx.y, lane = threadIdx.x & 31;
-  const int64_t n = P.ctl.n_store[r];
-  const int64_t base = (int64_t)r * P.stride;
-  const uint32_t* K = P.key + base;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  for (int64_t i0w = w * 128; i0w < n; i0w += nw * 128) {
+  const int64_t items_per_run = (P.cap + 1023) / 1024;
+  const int64_t n_items = items_per_run * P.R;
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int r = (int)(item / items_per_run);
+    const int64_t n = P.ctl.n_store[r];
+    const int64_t i0w = (item - (int64_t)r * items_per_run) * 1024 + (threadIdx.x >> 5) * 128;
+    if (i0w - (threadIdx.x >> 5) * 128 >= n) continue;
+    const int64_t base = (int64_t)r * P.stride;
+    const uint32_t* K = P.key + base;
     uint32_t kk[4], m[4], p0[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
@@ -664,6 +672,48 @@ __device__ __forceinline__ void collide_cell(const Prm& P, uint2 key, uint32_t c
   if (maxseen > gm) gmax = (float)maxseen;
 }
 
+// NTC, split for lane efficiency inside k_collide's shared-memory path:
+// ntc_count() draws M for a cell; the pair draws of all candidates of the tile
+// are then computed lane-parallel (E1) and ntc_apply() walks one cell's
+// candidates in increasing k (E2), exactly the order of collide_cell().
+__device__ __forceinline__ uint32_t ntc_count(const Prm& P, uint2 key, uint32_t c, uint32_t s, uint32_t N, float gmax) {
+  if (N < 2) return 0;
+  const double x = ((double)((int64_t)N * (int64_t)(N - 1)) * 0.5) * P.coef * (double)gmax;
+  const uint4 w = draw(key, c, s, TAG_COLL_COUNT, 0, 0);
+  int64_t M = (int64_t)floor(x + u_co_d(w.x));
+  if (M > 0xFFFFFF) { latch(P, ST_CELL); M = 0xFFFFFF; }
+  return (uint32_t)M;
+}
+
+// candidates k in [k_lo, k_hi) of one cell, pre-drawn: ij = i | j << 16, ur = raw word
+template <class A>
+__device__ __forceinline__ void ntc_apply(const Prm& P, uint2 key, uint32_t c, uint32_t s, const A& acc, double gm,
+                                          const uint32_t* ij, const uint32_t* ur, uint32_t k_lo, uint32_t k_hi,
+                                          double& maxseen, uint32_t& nacc) {
+  for (uint32_t k = k_lo; k < k_hi; k++) {
+    const uint32_t pr = ij[k - k_lo];
+    const uint32_t i = pr & 0xFFFFu, j = pr >> 16;
+    float a[3], b[3];
+    acc.ld(i, a);
+    acc.ld(j, b);
+    const float dx = a[0] - b[0], dy = a[1] - b[1], dz = a[2] - b[2];
+    const float g2 = (dx * dx + dy * dy) + dz * dz;
+    const double sg = P.model == 0 ? P.sigma_c * sqrt((double)g2) : P.sigma_c * pow((double)g2, P.omega1);
+    if (sg > maxseen) maxseen = sg;
+    if (u_co_d(ur[k - k_lo]) * gm < sg) {
+      float e[3];
+      marsaglia(key, c, s, k, e);
+      const float cmx = (a[0] + b[0]) * 0.5f, cmy = (a[1] + b[1]) * 0.5f, cmz = (a[2] + b[2]) * 0.5f;
+      const float hh = 0.5f * sqrtf(g2);
+      const float pa[3] = {cmx + hh * e[0], cmy + hh * e[1], cmz + hh * e[2]};
+      const float pb[3] = {cmx - hh * e[0], cmy - hh * e[1], cmz - hh * e[2]};
+      acc.st(i, pa);
+      acc.st(j, pb);
+      nacc++;
+    }
+  }
+}
+
 template <class A>
 __device__ __forceinline__ void sample_cell(const Prm& P, int slot, int64_t k, uint32_t N, const A& acc) {
   double sx = 0.0, sy = 0.0, sz = 0.0, se = 0.0;
@@ -706,6 +756,7 @@ __device__ void heap_sort(uint32_t* a, uint32_t n) {
 
 constexpr int CT = 128;     // cells per tile = threads per block
 constexpr int CAP = 1536;   // particles per tile staged in shared memory
+constexpr int CCAP = 512;   // NTC candidates per pre-draw round
 
 // One block = a tile of CT consecutive (run, cell) keys; thread t owns cell t.
 // mode 0: full step (collide, sample on sample steps, reorder); mode 1:
@@ -724,7 +775,10 @@ __global__ void __launch_bounds__(CT, 7) k_collide(Prm P, int mode, int slot_arg
   __shared__ uint8_t s_cell[CAP], s_mod[CAP];
   __shared__ uint32_t s_st[CT], s_n[CT], s_base[CT];
   __shared__ uint8_t s_ro[CT], s_h[CT], s_reo[CT];
-  __shared__ uint32_t s_S, s_E;
+  __shared__ uint32_t s_S, s_E, s_ntot;
+  __shared__ uint32_t s_mst[CT + 1];       // exclusive prefix of candidates per cell
+  __shared__ uint32_t s_cij[CCAP], s_cur[CCAP];
+  __shared__ uint32_t s_warp[CT / 32];
   const int t = threadIdx.x;
   const int64_t RN = (int64_t)P.R * P.Nc;
   const int64_t k0 = (int64_t)blockIdx.x * CT;
@@ -777,8 +831,11 @@ __global__ void __launch_bounds__(CT, 7) k_collide(Prm P, int mode, int slot_arg
       const int cq = s_cell[q];
       const uint32_t b = s_st[cq] - S, n = s_n[cq];
       const uint32_t v = s_a[q];
-      uint32_t rank = 0;
-      for (uint32_t p = 0; p < n; p++) rank += s_a[b + p] < v ? 1u : 0u;
+      uint32_t rank = 0, p = 0;
+      for (; p + 4 <= n; p += 4)
+        rank += (s_a[b + p] < v ? 1u : 0u) + (s_a[b + p + 1] < v ? 1u : 0u) + (s_a[b + p + 2] < v ? 1u : 0u) +
+                (s_a[b + p + 3] < v ? 1u : 0u);
+      for (; p < n; p++) rank += s_a[b + p] < v ? 1u : 0u;
       s_sorted[b + rank] = v;
     }
     __syncthreads();
@@ -803,12 +860,51 @@ __global__ void __launch_bounds__(CT, 7) k_collide(Prm P, int mode, int slot_arg
       s_mod[q] = 0;
     }
     __syncthreads();
-    // E
-    if (valid) {
-      SmemCell A{s_vx + off, s_vy + off, s_vz + off, s_mod + off};
-      if (collide) collide_cell(P, key, c, (uint32_t)s, N, A, gm, ncand, nacc);
-      if (slot >= 0) sample_cell(P, slot, k, N, A);
+    // E: NTC.  E0 candidate counts + block prefix; then rounds of E1 (pair
+    // draws of up to CCAP candidates, lane-parallel) and E2 (each thread walks
+    // its own cell's candidates of the round in increasing k)
+    SmemCell A{s_vx + off, s_vy + off, s_vz + off, s_mod + off};
+    if (collide) {
+      const uint32_t M = valid ? ntc_count(P, key, c, (uint32_t)s, N, gm) : 0u;
+      ncand = M;
+      uint32_t tot;
+      const uint32_t mst = block_excl_scan(M, s_warp, tot);
+      s_mst[t] = mst;
+      if (t == CT - 1) s_mst[CT] = mst + M;
+      const double gmd = (double)gm;
+      double maxseen = 0.0;
+      __syncthreads();
+      for (uint32_t base = 0; base < tot; base += CCAP) {
+        const uint32_t lim = tot - base < (uint32_t)CCAP ? tot - base : (uint32_t)CCAP;
+        for (uint32_t q = t; q < lim; q += CT) {
+          const uint32_t gq = base + q;
+          // cell of candidate gq: last cc with s_mst[cc] <= gq
+          int lo = 0, hi = CT;
+          while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (s_mst[mid] <= gq) lo = mid; else hi = mid; }
+          const int64_t kc = k0 + lo;
+          const int rc = (int)(kc / P.Nc);
+          const uint32_t cc = (uint32_t)(kc - (int64_t)rc * P.Nc);
+          const uint32_t nc = s_n[lo];
+          const uint4 w = draw(run_key(P, rc), cc, (uint32_t)s, TAG_COLL_PAIR, gq - s_mst[lo], 0);
+          const uint32_t i = lemire(w.x, nc);
+          uint32_t j = lemire(w.y, nc - 1);
+          if (j >= i) j++;
+          s_cij[q] = i | (j << 16);
+          s_cur[q] = w.z;
+        }
+        __syncthreads();
+        if (valid && M) {
+          const uint32_t a0 = mst > base ? mst : base;
+          const uint32_t a1 = mst + M < base + lim ? mst + M : base + lim;
+          if (a0 < a1)
+            ntc_apply(P, key, c, (uint32_t)s, A, gmd, s_cij + (a0 - base), s_cur + (a0 - base), a0 - mst, a1 - mst,
+                      maxseen, nacc);
+        }
+        __syncthreads();
+      }
+      if (maxseen > gmd) gm = (float)maxseen;
     }
+    if (valid && slot >= 0) sample_cell(P, slot, k, N, A);
     __syncthreads();
     // F
     for (uint32_t q = t; q < cnt; q += CT) {
@@ -980,13 +1076,12 @@ static void motion_t(const Prm& P, int mode, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_motion<D, EV>, 256, 0);
     if (occ < 1) occ = 1;
   }
-  int64_t want = (int64_t)num_sms() * occ;
-  int64_t per_run = (want + P.R - 1) / P.R;
-  const int64_t need = (P.cap + 1023) / 1024;
-  if (per_run > need) per_run = need;
-  if (per_run < 1) per_run = 1;
-  dim3 g((unsigned)per_run, (unsigned)P.R);
-  k_motion<D, EV><<<g, 256, 0, st>>>(P, mode);
+  // persistent: one wave of resident blocks walks the (run-major) items, so
+  // the cell counters being hit at any moment belong to one or two runs
+  const int64_t items = (P.cap + 1023) / 1024 * P.R;
+  int64_t g = (int64_t)num_sms() * occ;
+  if (g > items) g = items;
+  k_motion<D, EV><<<(unsigned)g, 256, 0, st>>>(P, mode);
 }
 
 void launch_motion(const Prm& P, int mode, cudaStream_t st) {
@@ -1007,13 +1102,10 @@ void launch_scatter(const Prm& P, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter, 256, 0);
     if (occ < 1) occ = 1;
   }
-  int64_t want = (int64_t)num_sms() * occ;
-  int64_t per_run = (want + P.R - 1) / P.R;
-  const int64_t need = (P.cap + 1023) / 1024;
-  if (per_run > need) per_run = need;
-  if (per_run < 1) per_run = 1;
-  dim3 g((unsigned)per_run, (unsigned)P.R);
-  k_scatter<<<g, 256, 0, st>>>(P);
+  const int64_t items = (P.cap + 1023) / 1024 * P.R;
+  int64_t g = (int64_t)num_sms() * occ;
+  if (g > items) g = items;
+  k_scatter<<<(unsigned)g, 256, 0, st>>>(P);
 }
 
 void launch_inflow(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
