@@ -267,6 +267,16 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   P.sqrt_inflowT = std::sqrt(p->inflow_T > 0 ? p->inflow_T : 1.0);
   if (p->inflow_kind == DSMC_INFLOW_GHOST) P.insert_bound = (int64_t)L.n_face * (int64_t)std::ceil(P.ghost_x);
   else if (p->inflow_kind == DSMC_INFLOW_EFFUSIVE) P.insert_bound = (int64_t)L.n_face * p->inflow_count;
+  {  // mean initial particles per cell decides the register sorting-network width
+    double filled = 0.0;
+    for (int k = 0; k < p->n_fill; k++) {
+      double vol = 1.0;
+      for (int a = 0; a < 3; a++) vol *= (double)(p->fill[k].hi[a] - p->fill[k].lo[a]);
+      filled += vol * p->fill[k].ppc;
+    }
+    const double ppc = filled / (double)L.Nc;
+    P.net_wide = (ppc > 12.0 || p->inflow_kind == DSMC_INFLOW_EFFUSIVE) ? 1 : 0;
+  }
   P.n_fill = p->n_fill;
   for (int k = 0; k < p->n_fill; k++) {
     for (int a = 0; a < 3; a++) {

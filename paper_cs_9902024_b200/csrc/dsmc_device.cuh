@@ -87,6 +87,7 @@ struct Prm {
   uint32_t* scan_part;       // scan tile partials
   double* macros;            // [Nc][10] staging
   int32_t debug;
+  int32_t net_wide;          // k_collide sorts segments of <= 32 (else 16) in registers
   int64_t* dbg_cand;         // [R*Nc]
   int32_t* dbg_acc;          // [R*Nc]
   Ctl ctl;

@@ -685,13 +685,32 @@ __device__ __forceinline__ uint32_t ntc_count(const Prm& P, uint2 key, uint32_t 
   return (uint32_t)M;
 }
 
-// candidates k in [k_lo, k_hi) of one cell, pre-drawn: ij = i | j << 16, ur = raw word
+// the Marsaglia pair (p, q) of candidate k (reading R14), drawn ahead of use
+__device__ __forceinline__ void marsaglia_pq(uint2 key, uint32_t c, uint32_t s, uint32_t k, float& pp_out,
+                                             float& qq_out) {
+  for (uint32_t blk = 0; blk < 64; blk++) {
+    const uint4 w = draw(key, c, s, TAG_COLL_DIR, k, blk);
+    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const float pp = 2.0f * u_co(ww[2 * h]) - 1.0f;
+      const float qq = 2.0f * u_co(ww[2 * h + 1]) - 1.0f;
+      const float rho = pp * pp + qq * qq;
+      if (rho < 1.0f) { pp_out = pp; qq_out = qq; return; }
+    }
+  }
+  pp_out = 0.0f;   // never reached in practice; gives e = (0, 0, 1) like marsaglia()
+  qq_out = 0.0f;
+}
+
+// candidates k in [k_lo, k_hi) of one cell, pre-drawn: ij = i | j << 16,
+// ur = raw acceptance word, (pp, qq) = Marsaglia pair
 template <class A>
-__device__ __forceinline__ void ntc_apply(const Prm& P, uint2 key, uint32_t c, uint32_t s, const A& acc, double gm,
-                                          const uint32_t* ij, const uint32_t* ur, uint32_t k_lo, uint32_t k_hi,
-                                          double& maxseen, uint32_t& nacc) {
-  for (uint32_t k = k_lo; k < k_hi; k++) {
-    const uint32_t pr = ij[k - k_lo];
+__device__ __forceinline__ void ntc_apply(const Prm& P, const A& acc, double gm, const uint32_t* ij, const uint32_t* ur,
+                                          const float* cp, const float* cq, uint32_t n, double& maxseen,
+                                          uint32_t& nacc) {
+  for (uint32_t k = 0; k < n; k++) {
+    const uint32_t pr = ij[k];
     const uint32_t i = pr & 0xFFFFu, j = pr >> 16;
     float a[3], b[3];
     acc.ld(i, a);
@@ -700,9 +719,11 @@ __device__ __forceinline__ void ntc_apply(const Prm& P, uint2 key, uint32_t c, u
     const float g2 = (dx * dx + dy * dy) + dz * dz;
     const double sg = P.model == 0 ? P.sigma_c * sqrt((double)g2) : P.sigma_c * pow((double)g2, P.omega1);
     if (sg > maxseen) maxseen = sg;
-    if (u_co_d(ur[k - k_lo]) * gm < sg) {
-      float e[3];
-      marsaglia(key, c, s, k, e);
+    if (u_co_d(ur[k]) * gm < sg) {
+      const float pp = cp[k], qq = cq[k];
+      const float rho = pp * pp + qq * qq;
+      const float sr = sqrtf(1.0f - rho);
+      const float e[3] = {2.0f * pp * sr, 2.0f * qq * sr, 1.0f - 2.0f * rho};
       const float cmx = (a[0] + b[0]) * 0.5f, cmy = (a[1] + b[1]) * 0.5f, cmz = (a[2] + b[2]) * 0.5f;
       const float hh = 0.5f * sqrtf(g2);
       const float pa[3] = {cmx + hh * e[0], cmy + hh * e[1], cmz + hh * e[2]};
@@ -710,6 +731,27 @@ __device__ __forceinline__ void ntc_apply(const Prm& P, uint2 key, uint32_t c, u
       acc.st(i, pa);
       acc.st(j, pb);
       nacc++;
+    }
+  }
+}
+
+// in-register bitonic sorting network (ascending), NN a power of two
+template <int NN>
+__device__ __forceinline__ void sort_net(uint32_t (&a)[NN]) {
+#pragma unroll
+  for (int k = 2; k <= NN; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < NN; i++) {
+        const int l = i ^ j;
+        if (l > i) {
+          const uint32_t x = a[i], y = a[l];
+          const bool asc = (i & k) == 0;
+          a[i] = asc ? min(x, y) : max(x, y);
+          a[l] = asc ? max(x, y) : min(x, y);
+        }
+      }
     }
   }
 }
@@ -767,8 +809,8 @@ constexpr int CCAP = 512;   // NTC candidates per pre-draw round
 //   D  gather velocities in canonical order; reorder: copy positions
 //   E  NTC per cell (thread per cell) + Sampling
 //   F  write modified velocities back (or the whole tile, reordered)
-template <int D>
-__global__ void __launch_bounds__(CT, 7) k_collide(Prm P, int mode, int slot_arg) {
+template <int D, int NET>
+__global__ void __launch_bounds__(CT, 6) k_collide(Prm P, int mode, int slot_arg) {
   __shared__ uint32_t s_sorted[CAP];
   __shared__ uint32_t s_a[CAP];       // raw LCR slice, then vx bits
   __shared__ float s_vy[CAP], s_vz[CAP];
@@ -778,9 +820,12 @@ __global__ void __launch_bounds__(CT, 7) k_collide(Prm P, int mode, int slot_arg
   __shared__ uint32_t s_S, s_E, s_ntot;
   __shared__ uint32_t s_mst[CT + 1];       // exclusive prefix of candidates per cell
   __shared__ uint32_t s_cij[CCAP], s_cur[CCAP];
+  __shared__ float s_cp[CCAP], s_cq[CCAP];
   __shared__ uint32_t s_warp[CT / 32];
   const int t = threadIdx.x;
   const int64_t RN = (int64_t)P.R * P.Nc;
+  const int64_t RS = (int64_t)P.R * P.stride;
+  float* const PH[2] = {P.P, P.P + P.half};
   const int64_t k0 = (int64_t)blockIdx.x * CT;
   const int64_t k = k0 + t;
   const bool valid = k < RN;
@@ -826,16 +871,25 @@ __global__ void __launch_bounds__(CT, 7) k_collide(Prm P, int mode, int slot_arg
     for (uint32_t q = t; q < cnt; q += CT) s_a[q] = P.lcr[S + q];
     if (valid) for (uint32_t i = 0; i < N; i++) s_cell[off + i] = (uint8_t)t;
     __syncthreads();
-    // C: values are distinct store indices -> rank = #smaller in the segment
+    // C: canonical order.  Segments of <= NET elements: the owning thread
+    // sorts them in registers (bitonic network); bigger ones: every element
+    // computes its rank (values are distinct store indices).
+    if (valid && N <= (uint32_t)NET) {
+      uint32_t v[NET];
+#pragma unroll
+      for (int i = 0; i < NET; i++) v[i] = (uint32_t)i < N ? s_a[off + i] : 0xFFFFFFFFu;
+      sort_net<NET>(v);
+#pragma unroll
+      for (int i = 0; i < NET; i++) if ((uint32_t)i < N) s_sorted[off + i] = v[i];
+    }
     for (uint32_t q = t; q < cnt; q += CT) {
       const int cq = s_cell[q];
-      const uint32_t b = s_st[cq] - S, n = s_n[cq];
+      const uint32_t n = s_n[cq];
+      if (n <= (uint32_t)NET) continue;
+      const uint32_t b = s_st[cq] - S;
       const uint32_t v = s_a[q];
-      uint32_t rank = 0, p = 0;
-      for (; p + 4 <= n; p += 4)
-        rank += (s_a[b + p] < v ? 1u : 0u) + (s_a[b + p + 1] < v ? 1u : 0u) + (s_a[b + p + 2] < v ? 1u : 0u) +
-                (s_a[b + p + 3] < v ? 1u : 0u);
-      for (; p < n; p++) rank += s_a[b + p] < v ? 1u : 0u;
+      uint32_t rank = 0;
+      for (uint32_t p = 0; p < n; p++) rank += s_a[b + p] < v ? 1u : 0u;
       s_sorted[b + rank] = v;
     }
     __syncthreads();
@@ -845,14 +899,16 @@ __global__ void __launch_bounds__(CT, 7) k_collide(Prm P, int mode, int slot_arg
       const uint32_t g = s_sorted[q];
       const int ro = s_ro[s_cell[q]];
       const int h = s_h[ro];
-      const float vx = parr(P, h, 3)[g], vy = parr(P, h, 4)[g], vz = parr(P, h, 5)[g];
+      const float* src = PH[h] + g;
+      const float vx = src[3 * RS], vy = src[4 * RS], vz = src[5 * RS];
       if (s_reo[ro]) {
         const int64_t dst = (int64_t)(r_first + ro) * P.stride + (int64_t)(S + q - s_base[ro]);
         float xs[D];
 #pragma unroll
-        for (int a = 0; a < D; a++) xs[a] = parr(P, h, a)[g];
+        for (int a = 0; a < D; a++) xs[a] = src[a * RS];
+        float* d = PH[h ^ 1] + dst;
 #pragma unroll
-        for (int a = 0; a < D; a++) parr(P, h ^ 1, a)[dst] = xs[a];
+        for (int a = 0; a < D; a++) d[a * RS] = xs[a];
       }
       s_vx[q] = vx;
       s_vy[q] = vy;
@@ -885,20 +941,23 @@ __global__ void __launch_bounds__(CT, 7) k_collide(Prm P, int mode, int slot_arg
           const int rc = (int)(kc / P.Nc);
           const uint32_t cc = (uint32_t)(kc - (int64_t)rc * P.Nc);
           const uint32_t nc = s_n[lo];
-          const uint4 w = draw(run_key(P, rc), cc, (uint32_t)s, TAG_COLL_PAIR, gq - s_mst[lo], 0);
+          const uint32_t kq = gq - s_mst[lo];
+          const uint2 keyc = run_key(P, rc);
+          const uint4 w = draw(keyc, cc, (uint32_t)s, TAG_COLL_PAIR, kq, 0);
           const uint32_t i = lemire(w.x, nc);
           uint32_t j = lemire(w.y, nc - 1);
           if (j >= i) j++;
           s_cij[q] = i | (j << 16);
           s_cur[q] = w.z;
+          marsaglia_pq(keyc, cc, (uint32_t)s, kq, s_cp[q], s_cq[q]);
         }
         __syncthreads();
         if (valid && M) {
           const uint32_t a0 = mst > base ? mst : base;
           const uint32_t a1 = mst + M < base + lim ? mst + M : base + lim;
           if (a0 < a1)
-            ntc_apply(P, key, c, (uint32_t)s, A, gmd, s_cij + (a0 - base), s_cur + (a0 - base), a0 - mst, a1 - mst,
-                      maxseen, nacc);
+            ntc_apply(P, A, gmd, s_cij + (a0 - base), s_cur + (a0 - base), s_cp + (a0 - base), s_cq + (a0 - base),
+                      a1 - a0, maxseen, nacc);
         }
         __syncthreads();
       }
@@ -913,13 +972,15 @@ __global__ void __launch_bounds__(CT, 7) k_collide(Prm P, int mode, int slot_arg
       const int h = s_h[ro];
       if (s_reo[ro]) {
         const int64_t dst = (int64_t)(r_first + ro) * P.stride + (int64_t)(S + q - s_base[ro]);
-        parr(P, h ^ 1, 3)[dst] = s_vx[q];
-        parr(P, h ^ 1, 4)[dst] = s_vy[q];
-        parr(P, h ^ 1, 5)[dst] = s_vz[q];
+        float* d = PH[h ^ 1] + dst;
+        d[3 * RS] = s_vx[q];
+        d[4 * RS] = s_vy[q];
+        d[5 * RS] = s_vz[q];
       } else if (s_mod[q]) {
-        parr(P, h, 3)[g] = s_vx[q];
-        parr(P, h, 4)[g] = s_vy[q];
-        parr(P, h, 5)[g] = s_vz[q];
+        float* d = PH[h] + g;
+        d[3 * RS] = s_vx[q];
+        d[4 * RS] = s_vy[q];
+        d[5 * RS] = s_vz[q];
       }
       if (P.debug) P.lcr[S + q] = g;
     }
@@ -1126,9 +1187,15 @@ void launch_step_mid(const Prm& P, cudaStream_t st) {
 void launch_collide(const Prm& P, int mode, int slot, cudaStream_t st) {
   const int64_t RN = (int64_t)P.R * P.Nc;
   const unsigned g = (unsigned)((RN + CT - 1) / CT);
-  if (P.dim == 1) k_collide<1><<<g, CT, 0, st>>>(P, mode, slot);
-  else if (P.dim == 2) k_collide<2><<<g, CT, 0, st>>>(P, mode, slot);
-  else k_collide<3><<<g, CT, 0, st>>>(P, mode, slot);
+  // register sorting network width: 16 for sparse cells, 32 for dense ones
+  const bool wide = P.net_wide != 0;
+  if (P.dim == 1) {
+    if (wide) k_collide<1, 32><<<g, CT, 0, st>>>(P, mode, slot); else k_collide<1, 16><<<g, CT, 0, st>>>(P, mode, slot);
+  } else if (P.dim == 2) {
+    if (wide) k_collide<2, 32><<<g, CT, 0, st>>>(P, mode, slot); else k_collide<2, 16><<<g, CT, 0, st>>>(P, mode, slot);
+  } else {
+    if (wide) k_collide<3, 32><<<g, CT, 0, st>>>(P, mode, slot); else k_collide<3, 16><<<g, CT, 0, st>>>(P, mode, slot);
+  }
 }
 
 void launch_step_end(const Prm& P, int mode, int slot, cudaStream_t st) {
