@@ -502,10 +502,14 @@ static void marsaglia(const orc_run* R, uint32_t c, uint32_t s, uint32_t k, floa
 }
 
 /* NTC collisions in one cell (Bird's no-time-counter scheme, cited by the
- * paper at PAPER.md:48,93; readings R12-R15 = SURVEY C-8):
+ * paper at PAPER.md:48,93; readings R12-R15 = SURVEY C-8, R13 as amended):
  *   M = floor(1/2 N (N-1) F_N/V_c (sigma g)_max dt + u)
- *   candidate k: i = lemire(a,N), j = lemire(b,N-1) (+1 if >= i), accept iff
- *   u_r (sigma g)_max < sigma g (fp64), g_max frozen during the step.
+ *   candidate k: i = lemire(a,N), j = lemire(b,N-1) (+1 if >= i);
+ *   accept with probability sigma(g) g / (sigma g)_max, decided in fp64:
+ *     HS : (u * ghat)^2 < g^2, ghat = (sigma g)_max / (pi d^2)   [no sqrt]
+ *     VHS: u (sigma g)_max < sigma_c (g^2)^(1-omega)
+ *   (sigma g)_max is frozen during the step; afterwards it becomes
+ *   max((sigma g)_max, sigma g(max g^2)) (sigma g is monotone in g^2).
  * vel[] are the cell's particles in canonical order; returns accepted count. */
 static int64_t interact(orc_run* R, int64_t c, int32_t s, int32_t N, float* vx, float* vy, float* vz,
                         float* gmax_c, int32_t* pairs, int64_t max_pairs, int64_t* n_cand) {
@@ -518,7 +522,8 @@ static int64_t interact(orc_run* R, int64_t c, int32_t s, int32_t N, float* vx, 
   int64_t M = (int64_t)floor(x + u_co_d(w[0]));
   if (M > 0xFFFFFF) { latch(R, ORC_EPARAM); M = 0xFFFFFF; }
   *n_cand = M;
-  double maxseen = 0.0;
+  const double ghat = gm / R->sigma_c;
+  float maxg2 = 0.0f;
   int64_t acc = 0;
   for (int64_t k = 0; k < M; k++) {
     draw(R, (uint32_t)c, (uint32_t)s, TAG_COLL_PAIR, (uint32_t)k, 0, w);
@@ -527,9 +532,15 @@ static int64_t interact(orc_run* R, int64_t c, int32_t s, int32_t N, float* vx, 
     if (j >= i) j++;
     float dx = vx[i] - vx[j], dy = vy[i] - vy[j], dz = vz[i] - vz[j];
     float g2 = (dx * dx + dy * dy) + dz * dz;
-    double sg = sigma_g(R, g2);
-    if (sg > maxseen) maxseen = sg;
-    if (u_co_d(w[2]) * gm < sg) {
+    if (g2 > maxg2) maxg2 = g2;
+    int accept;
+    if (R->p.model == ORC_HS) {
+      double lhs = u_co_d(w[2]) * ghat;
+      accept = lhs * lhs < (double)g2;
+    } else {
+      accept = u_co_d(w[2]) * gm < sigma_g(R, g2);
+    }
+    if (accept) {
       float e[3];
       marsaglia(R, (uint32_t)c, (uint32_t)s, (uint32_t)k, e);
       float cmx = (vx[i] + vx[j]) * 0.5f, cmy = (vy[i] + vy[j]) * 0.5f, cmz = (vz[i] + vz[j]) * 0.5f;
@@ -540,7 +551,10 @@ static int64_t interact(orc_run* R, int64_t c, int32_t s, int32_t N, float* vx, 
       acc++;
     }
   }
-  if (maxseen > gm) *gmax_c = (float)maxseen;
+  if (M > 0) {
+    double sgmax = sigma_g(R, maxg2);
+    if (sgmax > gm) *gmax_c = (float)sgmax;
+  }
   return acc;
 }
 
