@@ -639,11 +639,12 @@ __device__ __forceinline__ void collide_cell(const Prm& P, uint2 key, uint32_t c
   nacc = 0;
   if (N < 2) return;
   const double gm = (double)gmax;
+  const double ghat = gm / P.sigma_c;
   const double x = ((double)((int64_t)N * (int64_t)(N - 1)) * 0.5) * P.coef * gm;
   uint4 w = draw(key, c, s, TAG_COLL_COUNT, 0, 0);
   int64_t M = (int64_t)floor(x + u_co_d(w.x));
   if (M > 0xFFFFFF) { latch(P, ST_CELL); M = 0xFFFFFF; }
-  double maxseen = 0.0;
+  float maxg2 = 0.0f;
   for (uint32_t k = 0; k < (uint32_t)M; k++) {
     w = draw(key, c, s, TAG_COLL_PAIR, k, 0);
     const uint32_t i = lemire(w.x, N);
@@ -654,9 +655,15 @@ __device__ __forceinline__ void collide_cell(const Prm& P, uint2 key, uint32_t c
     acc.ld(j, b);
     const float dx = a[0] - b[0], dy = a[1] - b[1], dz = a[2] - b[2];
     const float g2 = (dx * dx + dy * dy) + dz * dz;
-    const double sg = P.model == 0 ? P.sigma_c * sqrt((double)g2) : P.sigma_c * pow((double)g2, P.omega1);
-    if (sg > maxseen) maxseen = sg;
-    if (u_co_d(w.z) * gm < sg) {
+    if (g2 > maxg2) maxg2 = g2;
+    bool accept;
+    if (P.model == 0) {
+      const double lhs = u_co_d(w.z) * ghat;
+      accept = lhs * lhs < (double)g2;
+    } else {
+      accept = u_co_d(w.z) * gm < P.sigma_c * pow((double)g2, P.omega1);
+    }
+    if (accept) {
       float e[3];
       marsaglia(key, c, s, k, e);
       const float cmx = (a[0] + b[0]) * 0.5f, cmy = (a[1] + b[1]) * 0.5f, cmz = (a[2] + b[2]) * 0.5f;
@@ -669,7 +676,10 @@ __device__ __forceinline__ void collide_cell(const Prm& P, uint2 key, uint32_t c
     }
   }
   ncand = (uint32_t)M;
-  if (maxseen > gm) gmax = (float)maxseen;
+  if (M > 0) {
+    const double sgm = P.model == 0 ? P.sigma_c * sqrt((double)maxg2) : P.sigma_c * pow((double)maxg2, P.omega1);
+    if (sgm > gm) gmax = (float)sgm;
+  }
 }
 
 // NTC, split for lane efficiency inside k_collide's shared-memory path:
@@ -706,9 +716,9 @@ __device__ __forceinline__ void marsaglia_pq(uint2 key, uint32_t c, uint32_t s, 
 // candidates k in [k_lo, k_hi) of one cell, pre-drawn: ij = i | j << 16,
 // ur = raw acceptance word, (pp, qq) = Marsaglia pair
 template <class A>
-__device__ __forceinline__ void ntc_apply(const Prm& P, const A& acc, double gm, const uint32_t* ij, const uint32_t* ur,
-                                          const float* cp, const float* cq, uint32_t n, double& maxseen,
-                                          uint32_t& nacc) {
+__device__ __forceinline__ void ntc_apply(const Prm& P, const A& acc, double gm, double ghat, const uint32_t* ij,
+                                          const uint32_t* ur, const float* cp, const float* cq, uint32_t n,
+                                          float& maxg2, uint32_t& nacc) {
   for (uint32_t k = 0; k < n; k++) {
     const uint32_t pr = ij[k];
     const uint32_t i = pr & 0xFFFFu, j = pr >> 16;
@@ -717,9 +727,15 @@ __device__ __forceinline__ void ntc_apply(const Prm& P, const A& acc, double gm,
     acc.ld(j, b);
     const float dx = a[0] - b[0], dy = a[1] - b[1], dz = a[2] - b[2];
     const float g2 = (dx * dx + dy * dy) + dz * dz;
-    const double sg = P.model == 0 ? P.sigma_c * sqrt((double)g2) : P.sigma_c * pow((double)g2, P.omega1);
-    if (sg > maxseen) maxseen = sg;
-    if (u_co_d(ur[k]) * gm < sg) {
+    maxg2 = g2 > maxg2 ? g2 : maxg2;
+    bool accept;
+    if (P.model == 0) {
+      const double lhs = u_co_d(ur[k]) * ghat;
+      accept = lhs * lhs < (double)g2;
+    } else {
+      accept = u_co_d(ur[k]) * gm < P.sigma_c * pow((double)g2, P.omega1);
+    }
+    if (accept) {
       const float pp = cp[k], qq = cq[k];
       const float rho = pp * pp + qq * qq;
       const float sr = sqrtf(1.0f - rho);
@@ -821,6 +837,9 @@ __global__ void __launch_bounds__(CT, 6) k_collide(Prm P, int mode, int slot_arg
   __shared__ uint32_t s_mst[CT + 1];       // exclusive prefix of candidates per cell
   __shared__ uint32_t s_cij[CCAP], s_cur[CCAP];
   __shared__ float s_cp[CCAP], s_cq[CCAP];
+  __shared__ float s_gm[CT], s_mg2[CT];
+  __shared__ uint32_t s_nacc[CT], s_bin[16];
+  __shared__ uint8_t s_perm[CT];
   __shared__ uint32_t s_warp[CT / 32];
   const int t = threadIdx.x;
   const int64_t RN = (int64_t)P.R * P.Nc;
@@ -830,15 +849,16 @@ __global__ void __launch_bounds__(CT, 6) k_collide(Prm P, int mode, int slot_arg
   const int64_t k = k0 + t;
   const bool valid = k < RN;
   const int64_t klast = (k0 + CT - 1 < RN ? k0 + CT - 1 : RN - 1);
-  const int r_first = (int)(k0 / P.Nc);
-  const int nr = (int)(klast / P.Nc) - r_first + 1;
+  const uint32_t Nc32 = (uint32_t)P.Nc;  // R*Nc < 2^31 (checked in dsmc_create)
+  const int r_first = (int)((uint32_t)k0 / Nc32);
+  const int nr = (int)((uint32_t)klast / Nc32) - r_first + 1;
   uint32_t st = 0, en = 0;
   if (valid) {
     st = k == 0 ? 0u : P.cell[k - 1];
     en = P.cell[k];
   }
-  const int r = valid ? (int)(k / P.Nc) : r_first;
-  const uint32_t c = valid ? (uint32_t)(k - (int64_t)r * P.Nc) : 0u;
+  const int r = valid ? (int)((uint32_t)k / Nc32) : r_first;
+  const uint32_t c = valid ? (uint32_t)k - (uint32_t)r * Nc32 : 0u;
   const uint32_t N = en - st;
   if (t == 0) s_S = st;
   if (k == klast) s_E = en;
@@ -863,6 +883,7 @@ __global__ void __launch_bounds__(CT, 6) k_collide(Prm P, int mode, int slot_arg
   uint32_t ncand = 0, nacc = 0;
   float gm = valid ? P.gmax[k] : 0.0f;
   const float gm0 = gm;
+  s_gm[t] = gm;
   __syncthreads();
   const uint32_t S = s_S, E = s_E, cnt = E - S;
   if (cnt <= (uint32_t)CAP) {
@@ -916,9 +937,11 @@ __global__ void __launch_bounds__(CT, 6) k_collide(Prm P, int mode, int slot_arg
       s_mod[q] = 0;
     }
     __syncthreads();
-    // E: NTC.  E0 candidate counts + block prefix; then rounds of E1 (pair
-    // draws of up to CCAP candidates, lane-parallel) and E2 (each thread walks
-    // its own cell's candidates of the round in increasing k)
+    // E: NTC.  E0: candidate counts M, block prefix, and a 16-bin counting
+    // sort of the cells by M (descending) so that each warp walks cells of
+    // similar M; then rounds of E1 (pair + direction draws of up to CCAP
+    // candidates, lane-parallel) and E2 (thread u walks the candidates of cell
+    // s_perm[u] in increasing k -- the sequential order of the method).
     SmemCell A{s_vx + off, s_vy + off, s_vz + off, s_mod + off};
     if (collide) {
       const uint32_t M = valid ? ntc_count(P, key, c, (uint32_t)s, N, gm) : 0u;
@@ -927,9 +950,29 @@ __global__ void __launch_bounds__(CT, 6) k_collide(Prm P, int mode, int slot_arg
       const uint32_t mst = block_excl_scan(M, s_warp, tot);
       s_mst[t] = mst;
       if (t == CT - 1) s_mst[CT] = mst + M;
-      const double gmd = (double)gm;
-      double maxseen = 0.0;
+      if (t < 16) s_bin[t] = 0;
       __syncthreads();
+      const uint32_t bin = 15u - (M < 15u ? M : 15u);
+      const uint32_t slot_in_bin = atomicAdd(&s_bin[bin], 1u);
+      __syncthreads();
+      if (t < 32) {  // exclusive scan of the 16 bin counts
+        uint32_t v = t < 16 ? s_bin[t] : 0u, x = v;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, x, o); if ((t & 31) >= o) x += y; }
+        if (t < 16) s_bin[t] = x - v;
+      }
+      __syncthreads();
+      s_perm[s_bin[bin] + slot_in_bin] = (uint8_t)t;
+      __syncthreads();
+      // this thread's assigned cell
+      const int u = s_perm[t];
+      const uint32_t Mu = s_mst[u + 1] - s_mst[u], mstu = s_mst[u];
+      const uint32_t offu = s_st[u] - S;
+      const double gmu = (double)s_gm[u];
+      const double ghatu = gmu / P.sigma_c;
+      SmemCell Au{s_vx + offu, s_vy + offu, s_vz + offu, s_mod + offu};
+      float maxg2 = 0.0f;
+      uint32_t naccu = 0;
       for (uint32_t base = 0; base < tot; base += CCAP) {
         const uint32_t lim = tot - base < (uint32_t)CCAP ? tot - base : (uint32_t)CCAP;
         for (uint32_t q = t; q < lim; q += CT) {
@@ -938,7 +981,7 @@ __global__ void __launch_bounds__(CT, 6) k_collide(Prm P, int mode, int slot_arg
           int lo = 0, hi = CT;
           while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (s_mst[mid] <= gq) lo = mid; else hi = mid; }
           const int64_t kc = k0 + lo;
-          const int rc = (int)(kc / P.Nc);
+          const int rc = r_first + s_ro[lo];
           const uint32_t cc = (uint32_t)(kc - (int64_t)rc * P.Nc);
           const uint32_t nc = s_n[lo];
           const uint32_t kq = gq - s_mst[lo];
@@ -952,16 +995,24 @@ __global__ void __launch_bounds__(CT, 6) k_collide(Prm P, int mode, int slot_arg
           marsaglia_pq(keyc, cc, (uint32_t)s, kq, s_cp[q], s_cq[q]);
         }
         __syncthreads();
-        if (valid && M) {
-          const uint32_t a0 = mst > base ? mst : base;
-          const uint32_t a1 = mst + M < base + lim ? mst + M : base + lim;
+        if (Mu) {
+          const uint32_t a0 = mstu > base ? mstu : base;
+          const uint32_t a1 = mstu + Mu < base + lim ? mstu + Mu : base + lim;
           if (a0 < a1)
-            ntc_apply(P, A, gmd, s_cij + (a0 - base), s_cur + (a0 - base), s_cp + (a0 - base), s_cq + (a0 - base),
-                      a1 - a0, maxseen, nacc);
+            ntc_apply(P, Au, gmu, ghatu, s_cij + (a0 - base), s_cur + (a0 - base), s_cp + (a0 - base),
+                      s_cq + (a0 - base), a1 - a0, maxg2, naccu);
         }
         __syncthreads();
       }
-      if (maxseen > gmd) gm = (float)maxseen;
+      s_mg2[u] = maxg2;
+      s_nacc[u] = naccu;
+      __syncthreads();
+      if (valid && M) {
+        nacc = s_nacc[t];
+        const float mg = s_mg2[t];
+        const double sgm = P.model == 0 ? P.sigma_c * sqrt((double)mg) : P.sigma_c * pow((double)mg, P.omega1);
+        if (sgm > (double)gm) gm = (float)sgm;
+      }
     }
     if (valid && slot >= 0) sample_cell(P, slot, k, N, A);
     __syncthreads();
