@@ -826,14 +826,14 @@ constexpr int CCAP = 512;   // NTC candidates per pre-draw round
 //   E  NTC per cell (thread per cell) + Sampling
 //   F  write modified velocities back (or the whole tile, reordered)
 template <int D, int NET>
-__global__ void __launch_bounds__(CT, 6) k_collide(Prm P, int mode, int slot_arg) {
+__global__ void __launch_bounds__(CT, 5) k_collide(Prm P, int mode, int slot_arg) {
   __shared__ uint32_t s_sorted[CAP];
   __shared__ uint32_t s_a[CAP];       // raw LCR slice, then vx bits
   __shared__ float s_vy[CAP], s_vz[CAP];
   __shared__ uint8_t s_cell[CAP], s_mod[CAP];
   __shared__ uint32_t s_st[CT], s_n[CT], s_base[CT];
   __shared__ uint8_t s_ro[CT], s_h[CT], s_reo[CT];
-  __shared__ uint32_t s_S, s_E, s_ntot;
+  __shared__ uint32_t s_S, s_E;
   __shared__ uint32_t s_mst[CT + 1];       // exclusive prefix of candidates per cell
   __shared__ uint32_t s_cij[CCAP], s_cur[CCAP];
   __shared__ float s_cp[CCAP], s_cq[CCAP];
@@ -844,7 +844,8 @@ __global__ void __launch_bounds__(CT, 6) k_collide(Prm P, int mode, int slot_arg
   const int t = threadIdx.x;
   const int64_t RN = (int64_t)P.R * P.Nc;
   const int64_t RS = (int64_t)P.R * P.stride;
-  float* const PH[2] = {P.P, P.P + P.half};
+  float* const P0 = P.P;
+  float* const P1 = P.P + P.half;
   const int64_t k0 = (int64_t)blockIdx.x * CT;
   const int64_t k = k0 + t;
   const bool valid = k < RN;
@@ -916,18 +917,20 @@ __global__ void __launch_bounds__(CT, 6) k_collide(Prm P, int mode, int slot_arg
     __syncthreads();
     // D
     float* s_vx = reinterpret_cast<float*>(s_a);
+    const bool one_run = nr == 1;           // common case: metadata is block-uniform
+    const int h1 = s_h[0], reo1 = s_reo[0];
     for (uint32_t q = t; q < cnt; q += CT) {
       const uint32_t g = s_sorted[q];
-      const int ro = s_ro[s_cell[q]];
-      const int h = s_h[ro];
-      const float* src = PH[h] + g;
+      int ro = 0, h = h1, reo = reo1;
+      if (!one_run) { ro = s_ro[s_cell[q]]; h = s_h[ro]; reo = s_reo[ro]; }
+      const float* src = (h ? P1 : P0) + g;
       const float vx = src[3 * RS], vy = src[4 * RS], vz = src[5 * RS];
-      if (s_reo[ro]) {
+      if (reo) {
         const int64_t dst = (int64_t)(r_first + ro) * P.stride + (int64_t)(S + q - s_base[ro]);
         float xs[D];
 #pragma unroll
         for (int a = 0; a < D; a++) xs[a] = src[a * RS];
-        float* d = PH[h ^ 1] + dst;
+        float* d = (h ? P0 : P1) + dst;
 #pragma unroll
         for (int a = 0; a < D; a++) d[a * RS] = xs[a];
       }
@@ -1018,22 +1021,21 @@ __global__ void __launch_bounds__(CT, 6) k_collide(Prm P, int mode, int slot_arg
     __syncthreads();
     // F
     for (uint32_t q = t; q < cnt; q += CT) {
-      const uint32_t g = s_sorted[q];
-      const int ro = s_ro[s_cell[q]];
-      const int h = s_h[ro];
-      if (s_reo[ro]) {
+      int ro = 0, h = h1, reo = reo1;
+      if (!one_run) { ro = s_ro[s_cell[q]]; h = s_h[ro]; reo = s_reo[ro]; }
+      if (reo) {
         const int64_t dst = (int64_t)(r_first + ro) * P.stride + (int64_t)(S + q - s_base[ro]);
-        float* d = PH[h ^ 1] + dst;
+        float* d = (h ? P0 : P1) + dst;
         d[3 * RS] = s_vx[q];
         d[4 * RS] = s_vy[q];
         d[5 * RS] = s_vz[q];
       } else if (s_mod[q]) {
-        float* d = PH[h] + g;
+        float* d = (h ? P1 : P0) + s_sorted[q];
         d[3 * RS] = s_vx[q];
         d[4 * RS] = s_vy[q];
         d[5 * RS] = s_vz[q];
       }
-      if (P.debug) P.lcr[S + q] = g;
+      if (P.debug) P.lcr[S + q] = s_sorted[q];
     }
   } else if (valid) {
     // tile too large for shared memory: this thread works on its own cell
