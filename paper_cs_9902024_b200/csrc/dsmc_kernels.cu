@@ -918,26 +918,56 @@ __global__ void __launch_bounds__(CT, 5) k_collide(Prm P, int mode, int slot_arg
     // D
     float* s_vx = reinterpret_cast<float*>(s_a);
     const bool one_run = nr == 1;           // common case: metadata is block-uniform
-    const int h1 = s_h[0], reo1 = s_reo[0];
-    for (uint32_t q = t; q < cnt; q += CT) {
-      const uint32_t g = s_sorted[q];
-      int ro = 0, h = h1, reo = reo1;
-      if (!one_run) { ro = s_ro[s_cell[q]]; h = s_h[ro]; reo = s_reo[ro]; }
-      const float* src = (h ? P1 : P0) + g;
-      const float vx = src[3 * RS], vy = src[4 * RS], vz = src[5 * RS];
-      if (reo) {
-        const int64_t dst = (int64_t)(r_first + ro) * P.stride + (int64_t)(S + q - s_base[ro]);
-        float xs[D];
+    if (one_run) {
+      const int h = s_h[0];
+      const float* __restrict__ sx = (h ? P1 : P0) + 3 * RS;
+      const float* __restrict__ sy = sx + RS;
+      const float* __restrict__ sz = sy + RS;
+      if (s_reo[0]) {
+        // reorder: positions move to the other half at their canonical rank
+        const float* __restrict__ px = (h ? P1 : P0);
+        float* __restrict__ dx = (h ? P0 : P1) + (int64_t)r_first * P.stride + (S - s_base[0]);
+        for (uint32_t q = t; q < cnt; q += CT) {
+          const uint32_t g = s_sorted[q];
+          float xs[D];
 #pragma unroll
-        for (int a = 0; a < D; a++) xs[a] = src[a * RS];
-        float* d = (h ? P0 : P1) + dst;
+          for (int a = 0; a < D; a++) xs[a] = px[a * RS + g];
+          s_vx[q] = sx[g];
+          s_vy[q] = sy[g];
+          s_vz[q] = sz[g];
+          s_mod[q] = 0;
 #pragma unroll
-        for (int a = 0; a < D; a++) d[a * RS] = xs[a];
+          for (int a = 0; a < D; a++) dx[a * RS + q] = xs[a];
+        }
+      } else {
+        for (uint32_t q = t; q < cnt; q += CT) {
+          const uint32_t g = s_sorted[q];
+          s_vx[q] = sx[g];
+          s_vy[q] = sy[g];
+          s_vz[q] = sz[g];
+          s_mod[q] = 0;
+        }
       }
-      s_vx[q] = vx;
-      s_vy[q] = vy;
-      s_vz[q] = vz;
-      s_mod[q] = 0;
+    } else {
+      for (uint32_t q = t; q < cnt; q += CT) {
+        const uint32_t g = s_sorted[q];
+        const int ro = s_ro[s_cell[q]], h = s_h[ro];
+        const float* src = (h ? P1 : P0) + g;
+        const float vx = src[3 * RS], vy = src[4 * RS], vz = src[5 * RS];
+        if (s_reo[ro]) {
+          const int64_t dst = (int64_t)(r_first + ro) * P.stride + (int64_t)(S + q - s_base[ro]);
+          float xs[D];
+#pragma unroll
+          for (int a = 0; a < D; a++) xs[a] = src[a * RS];
+          float* d = (h ? P0 : P1) + dst;
+#pragma unroll
+          for (int a = 0; a < D; a++) d[a * RS] = xs[a];
+        }
+        s_vx[q] = vx;
+        s_vy[q] = vy;
+        s_vz[q] = vz;
+        s_mod[q] = 0;
+      }
     }
     __syncthreads();
     // E: NTC.  E0: candidate counts M, block prefix, and a 16-bin counting
@@ -1020,23 +1050,45 @@ __global__ void __launch_bounds__(CT, 5) k_collide(Prm P, int mode, int slot_arg
     if (valid && slot >= 0) sample_cell(P, slot, k, N, A);
     __syncthreads();
     // F
-    for (uint32_t q = t; q < cnt; q += CT) {
-      int ro = 0, h = h1, reo = reo1;
-      if (!one_run) { ro = s_ro[s_cell[q]]; h = s_h[ro]; reo = s_reo[ro]; }
-      if (reo) {
-        const int64_t dst = (int64_t)(r_first + ro) * P.stride + (int64_t)(S + q - s_base[ro]);
-        float* d = (h ? P0 : P1) + dst;
-        d[3 * RS] = s_vx[q];
-        d[4 * RS] = s_vy[q];
-        d[5 * RS] = s_vz[q];
-      } else if (s_mod[q]) {
-        float* d = (h ? P1 : P0) + s_sorted[q];
-        d[3 * RS] = s_vx[q];
-        d[4 * RS] = s_vy[q];
-        d[5 * RS] = s_vz[q];
+    if (one_run) {
+      const int h = s_h[0];
+      if (s_reo[0]) {
+        float* __restrict__ dx = (h ? P0 : P1) + 3 * RS + (int64_t)r_first * P.stride + (S - s_base[0]);
+        for (uint32_t q = t; q < cnt; q += CT) {
+          dx[q] = s_vx[q];
+          dx[RS + q] = s_vy[q];
+          dx[2 * RS + q] = s_vz[q];
+        }
+      } else {
+        float* __restrict__ vxp = (h ? P1 : P0) + 3 * RS;
+        for (uint32_t q = t; q < cnt; q += CT) {
+          if (s_mod[q]) {
+            const uint32_t g = s_sorted[q];
+            vxp[g] = s_vx[q];
+            vxp[RS + g] = s_vy[q];
+            vxp[2 * RS + g] = s_vz[q];
+          }
+        }
       }
-      if (P.debug) P.lcr[S + q] = s_sorted[q];
+    } else {
+      for (uint32_t q = t; q < cnt; q += CT) {
+        const int ro = s_ro[s_cell[q]], h = s_h[ro];
+        if (s_reo[ro]) {
+          const int64_t dst = (int64_t)(r_first + ro) * P.stride + (int64_t)(S + q - s_base[ro]);
+          float* d = (h ? P0 : P1) + dst;
+          d[3 * RS] = s_vx[q];
+          d[4 * RS] = s_vy[q];
+          d[5 * RS] = s_vz[q];
+        } else if (s_mod[q]) {
+          float* d = (h ? P1 : P0) + s_sorted[q];
+          d[3 * RS] = s_vx[q];
+          d[4 * RS] = s_vy[q];
+          d[5 * RS] = s_vz[q];
+        }
+      }
     }
+    if (P.debug)
+      for (uint32_t q = t; q < cnt; q += CT) P.lcr[S + q] = s_sorted[q];
   } else if (valid) {
     // tile too large for shared memory: this thread works on its own cell
     // directly in global memory (segment sorted in place in LCR)
