@@ -2,6 +2,7 @@
 // include/dsmc.h).  Host logic only: validation, buffer layout, the step
 // graph, host<->device marshalling.  Every step of the method runs in the
 // kernels of dsmc_kernels.cu; there is no CPU fallback.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -276,6 +277,14 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
     }
     const double ppc = filled / (double)L.Nc;
     P.net_wide = (ppc > 12.0 || p->inflow_kind == DSMC_INFLOW_EFFUSIVE) ? 1 : 0;
+    // warp-tile staging capacity: the densest fill region's 32 cells with a
+    // wide margin (tiles beyond it take the per-lane global-memory path)
+    int32_t ppc_max = 0;
+    for (int k = 0; k < p->n_fill; k++) ppc_max = p->fill[k].ppc > ppc_max ? p->fill[k].ppc : ppc_max;
+    if (p->inflow_kind == DSMC_INFLOW_GHOST) ppc_max = std::max(ppc_max, (int32_t)std::ceil(p->inflow_n));
+    int32_t capw = 32 * ppc_max + 8 * (int32_t)std::ceil(std::sqrt(32.0 * ppc_max)) + 64;
+    capw = std::max(256, std::min(capw, 4096));
+    P.capw = (capw + 31) / 32 * 32;
   }
   P.n_fill = p->n_fill;
   for (int k = 0; k < p->n_fill; k++) {

@@ -812,69 +812,91 @@ __device__ void heap_sort(uint32_t* a, uint32_t n) {
   }
 }
 
-constexpr int CT = 128;     // cells per tile = threads per block
-constexpr int CAP = 1536;   // particles per tile staged in shared memory
-constexpr int CCAP = 512;   // NTC candidates per pre-draw round
+// ---------------------------------------------------------------------------
+// k_collide: Interaction + Sampling (+ physical reorder) for tiles of 32
+// consecutive (run, cell) keys.  Each WARP owns one tile independently (lane
+// = cell): per-cell scalars stay in registers and are exchanged by shuffles,
+// the tile's particles are staged in the warp's slice of shared memory, and
+// phases are separated by __syncwarp only, so the warps of an SM overlap
+// their memory and compute phases freely.
+//   A  segment bounds from the LCR ends, run metadata
+//   B  stage the tile's LCR slice; tag each position with its cell (lane)
+//   C  canonical order (R11): lanes sort segments of <= NET in registers
+//      (bitonic network); bigger segments rank every element
+//   D  gather velocities in canonical order; on reorder steps copy positions
+//      to their canonical rank in the other half of P
+//   E  NTC: M per cell, warp prefix, cells reassigned to lanes in order of M
+//      (bitonic over the warp); rounds of pre-drawn candidates (pair,
+//      acceptance word, Marsaglia pair), then each lane walks one cell's
+//      candidates in increasing k -- the method's sequential order
+//   F  write modified velocities back (or the whole tile to its new rank)
+// mode 0: full step; mode 1: sample only into `slot_arg` (dsmc_sample).
+constexpr int WPB = 4;      // warps per block
+constexpr int CCW = 128;    // pre-drawn candidates per round per warp
 
-// One block = a tile of CT consecutive (run, cell) keys; thread t owns cell t.
-// mode 0: full step (collide, sample on sample steps, reorder); mode 1:
-// sample only into `slot` (explicit dsmc_sample).
-//   A  segment bounds, per-run metadata (parity, reorder flag, LCR base)
-//   B  stage the tile's LCR slice; tag each position with its cell
-//   C  canonical order (R11): rank of each element inside its segment
-//   D  gather velocities in canonical order; reorder: copy positions
-//   E  NTC per cell (thread per cell) + Sampling
-//   F  write modified velocities back (or the whole tile, reordered)
+struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
+  uint32_t* sorted; uint32_t* a; float* vy; float* vz; uint8_t* cell; uint8_t* mod;
+  uint32_t* cij; uint32_t* cur; float* cp; float* cq; float* mg2; uint32_t* nacc;
+};
+
+__host__ __device__ inline size_t warp_smem_bytes(int capw) {
+  return (size_t)capw * 18 + (size_t)CCW * 16 + 32 * 8 + 16;
+}
+
+__device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
+  WarpSmem w;
+  w.sorted = reinterpret_cast<uint32_t*>(base);
+  w.a = w.sorted + capw;
+  w.vy = reinterpret_cast<float*>(w.a + capw);
+  w.vz = w.vy + capw;
+  w.cij = reinterpret_cast<uint32_t*>(w.vz + capw);
+  w.cur = w.cij + CCW;
+  w.cp = reinterpret_cast<float*>(w.cur + CCW);
+  w.cq = w.cp + CCW;
+  w.mg2 = w.cq + CCW;
+  w.nacc = reinterpret_cast<uint32_t*>(w.mg2 + 32);
+  w.cell = reinterpret_cast<uint8_t*>(w.nacc + 32);
+  w.mod = w.cell + capw;
+  return w;
+}
+
 template <int D, int NET>
-__global__ void __launch_bounds__(CT, 5) k_collide(Prm P, int mode, int slot_arg) {
-  __shared__ uint32_t s_sorted[CAP];
-  __shared__ uint32_t s_a[CAP];       // raw LCR slice, then vx bits
-  __shared__ float s_vy[CAP], s_vz[CAP];
-  __shared__ uint8_t s_cell[CAP], s_mod[CAP];
-  __shared__ uint32_t s_st[CT], s_n[CT], s_base[CT];
-  __shared__ uint8_t s_ro[CT], s_h[CT], s_reo[CT];
-  __shared__ uint32_t s_S, s_E;
-  __shared__ uint32_t s_mst[CT + 1];       // exclusive prefix of candidates per cell
-  __shared__ uint32_t s_cij[CCAP], s_cur[CCAP];
-  __shared__ float s_cp[CCAP], s_cq[CCAP];
-  __shared__ float s_gm[CT], s_mg2[CT];
-  __shared__ uint32_t s_nacc[CT], s_bin[16];
-  __shared__ uint8_t s_perm[CT];
-  __shared__ uint32_t s_warp[CT / 32];
-  const int t = threadIdx.x;
+__global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_arg, int capw) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const WarpSmem W = warp_smem(dsm + (size_t)wid * warp_smem_bytes(capw), capw);
   const int64_t RN = (int64_t)P.R * P.Nc;
   const int64_t RS = (int64_t)P.R * P.stride;
   float* const P0 = P.P;
   float* const P1 = P.P + P.half;
-  const int64_t k0 = (int64_t)blockIdx.x * CT;
-  const int64_t k = k0 + t;
+  const int64_t k0 = ((int64_t)blockIdx.x * WPB + wid) * 32;
+  if (k0 >= RN) return;                          // whole warp leaves together
+  const int64_t k = k0 + lane;
   const bool valid = k < RN;
-  const int64_t klast = (k0 + CT - 1 < RN ? k0 + CT - 1 : RN - 1);
-  const uint32_t Nc32 = (uint32_t)P.Nc;  // R*Nc < 2^31 (checked in dsmc_create)
+  const int64_t klast = k0 + 31 < RN ? k0 + 31 : RN - 1;
+  const int last_lane = (int)(klast - k0);
+  const uint32_t Nc32 = (uint32_t)P.Nc;          // R*Nc < 2^31 (checked in dsmc_create)
   const int r_first = (int)((uint32_t)k0 / Nc32);
-  const int nr = (int)((uint32_t)klast / Nc32) - r_first + 1;
+  const int r_last = (int)((uint32_t)klast / Nc32);
+  const bool one_run = r_first == r_last;
+  // ---- A
   uint32_t st = 0, en = 0;
   if (valid) {
     st = k == 0 ? 0u : P.cell[k - 1];
     en = P.cell[k];
   }
-  const int r = valid ? (int)((uint32_t)k / Nc32) : r_first;
+  const int r = valid ? (int)((uint32_t)k / Nc32) : r_last;
   const uint32_t c = valid ? (uint32_t)k - (uint32_t)r * Nc32 : 0u;
   const uint32_t N = en - st;
-  if (t == 0) s_S = st;
-  if (k == klast) s_E = en;
-  s_st[t] = st;
-  s_n[t] = N;
-  s_ro[t] = (uint8_t)(r - r_first);
-  if (t < nr) {
-    const int rr = r_first + t;
-    s_h[t] = (uint8_t)P.ctl.parity[rr];
-    s_reo[t] = (uint8_t)(mode == 0 ? P.ctl.reorder[rr] : 0);
-    s_base[t] = run_lcr_base(P, rr);
-  }
+  const uint32_t S = __shfl_sync(FULL, st, 0);
+  const uint32_t E = __shfl_sync(FULL, en, last_lane);
+  const uint32_t cnt = E - S;
+  const uint32_t off = st - S;
+  const int h = P.ctl.parity[r];
+  const int reo = mode == 0 ? P.ctl.reorder[r] : 0;
+  const uint32_t rbase = run_lcr_base(P, r);
   const int32_t s = *P.ctl.step;
   int slot = -1;
-  const bool collide = mode == 0;
   if (mode == 0) {
     if ((s + 1) % P.sample_every == 0 && (s + 1) / P.sample_every - 1 < P.n_slots) slot = (s + 1) / P.sample_every - 1;
   } else {
@@ -884,227 +906,219 @@ __global__ void __launch_bounds__(CT, 5) k_collide(Prm P, int mode, int slot_arg
   uint32_t ncand = 0, nacc = 0;
   float gm = valid ? P.gmax[k] : 0.0f;
   const float gm0 = gm;
-  s_gm[t] = gm;
-  __syncthreads();
-  const uint32_t S = s_S, E = s_E, cnt = E - S;
-  if (cnt <= (uint32_t)CAP) {
-    const uint32_t off = st - S;
-    // B
-    for (uint32_t q = t; q < cnt; q += CT) s_a[q] = P.lcr[S + q];
-    if (valid) for (uint32_t i = 0; i < N; i++) s_cell[off + i] = (uint8_t)t;
-    __syncthreads();
-    // C: canonical order.  Segments of <= NET elements: the owning thread
-    // sorts them in registers (bitonic network); bigger ones: every element
-    // computes its rank (values are distinct store indices).
+  if (cnt <= (uint32_t)capw) {
+    // ---- B
+    for (uint32_t q = lane; q < cnt; q += 32) W.a[q] = P.lcr[S + q];
+    if (valid) for (uint32_t i = 0; i < N; i++) W.cell[off + i] = (uint8_t)lane;
+    __syncwarp();
+    // ---- C
     if (valid && N <= (uint32_t)NET) {
       uint32_t v[NET];
 #pragma unroll
-      for (int i = 0; i < NET; i++) v[i] = (uint32_t)i < N ? s_a[off + i] : 0xFFFFFFFFu;
+      for (int i = 0; i < NET; i++) v[i] = (uint32_t)i < N ? W.a[off + i] : 0xFFFFFFFFu;
       sort_net<NET>(v);
 #pragma unroll
-      for (int i = 0; i < NET; i++) if ((uint32_t)i < N) s_sorted[off + i] = v[i];
+      for (int i = 0; i < NET; i++) if ((uint32_t)i < N) W.sorted[off + i] = v[i];
     }
-    for (uint32_t q = t; q < cnt; q += CT) {
-      const int cq = s_cell[q];
-      const uint32_t n = s_n[cq];
-      if (n <= (uint32_t)NET) continue;
-      const uint32_t b = s_st[cq] - S;
-      const uint32_t v = s_a[q];
-      uint32_t rank = 0;
-      for (uint32_t p = 0; p < n; p++) rank += s_a[b + p] < v ? 1u : 0u;
-      s_sorted[b + rank] = v;
+    if (__any_sync(FULL, valid && N > (uint32_t)NET)) {
+      for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        const int cq = q < cnt ? W.cell[q] : 0;
+        const uint32_t n = __shfl_sync(FULL, N, cq), b = __shfl_sync(FULL, off, cq);
+        if (q < cnt && n > (uint32_t)NET) {
+          const uint32_t v = W.a[q];
+          uint32_t rank = 0;
+          for (uint32_t p = 0; p < n; p++) rank += W.a[b + p] < v ? 1u : 0u;
+          W.sorted[b + rank] = v;
+        }
+      }
     }
-    __syncthreads();
-    // D
-    float* s_vx = reinterpret_cast<float*>(s_a);
-    const bool one_run = nr == 1;           // common case: metadata is block-uniform
+    __syncwarp();
+    // ---- D
+    float* const wvx = reinterpret_cast<float*>(W.a);
     if (one_run) {
-      const int h = s_h[0];
       const float* __restrict__ sx = (h ? P1 : P0) + 3 * RS;
-      const float* __restrict__ sy = sx + RS;
-      const float* __restrict__ sz = sy + RS;
-      if (s_reo[0]) {
-        // reorder: positions move to the other half at their canonical rank
+      if (reo) {
         const float* __restrict__ px = (h ? P1 : P0);
-        float* __restrict__ dx = (h ? P0 : P1) + (int64_t)r_first * P.stride + (S - s_base[0]);
-        for (uint32_t q = t; q < cnt; q += CT) {
-          const uint32_t g = s_sorted[q];
+        float* __restrict__ dx = (h ? P0 : P1) + (int64_t)r * P.stride + (S - rbase);
+        for (uint32_t q = lane; q < cnt; q += 32) {
+          const uint32_t g = W.sorted[q];
           float xs[D];
 #pragma unroll
           for (int a = 0; a < D; a++) xs[a] = px[a * RS + g];
-          s_vx[q] = sx[g];
-          s_vy[q] = sy[g];
-          s_vz[q] = sz[g];
-          s_mod[q] = 0;
+          wvx[q] = sx[g];
+          W.vy[q] = sx[RS + g];
+          W.vz[q] = sx[2 * RS + g];
+          W.mod[q] = 0;
 #pragma unroll
           for (int a = 0; a < D; a++) dx[a * RS + q] = xs[a];
         }
       } else {
-        for (uint32_t q = t; q < cnt; q += CT) {
-          const uint32_t g = s_sorted[q];
-          s_vx[q] = sx[g];
-          s_vy[q] = sy[g];
-          s_vz[q] = sz[g];
-          s_mod[q] = 0;
+        for (uint32_t q = lane; q < cnt; q += 32) {
+          const uint32_t g = W.sorted[q];
+          wvx[q] = sx[g];
+          W.vy[q] = sx[RS + g];
+          W.vz[q] = sx[2 * RS + g];
+          W.mod[q] = 0;
         }
       }
     } else {
-      for (uint32_t q = t; q < cnt; q += CT) {
-        const uint32_t g = s_sorted[q];
-        const int ro = s_ro[s_cell[q]], h = s_h[ro];
-        const float* src = (h ? P1 : P0) + g;
-        const float vx = src[3 * RS], vy = src[4 * RS], vz = src[5 * RS];
-        if (s_reo[ro]) {
-          const int64_t dst = (int64_t)(r_first + ro) * P.stride + (int64_t)(S + q - s_base[ro]);
-          float xs[D];
+      for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        const int cq = q < cnt ? W.cell[q] : 0;
+        const int hq = __shfl_sync(FULL, h, cq), rq = __shfl_sync(FULL, reo, cq);
+        const int runq = __shfl_sync(FULL, r, cq);
+        const uint32_t bq = __shfl_sync(FULL, rbase, cq);
+        if (q < cnt) {
+          const uint32_t g = W.sorted[q];
+          const float* src = (hq ? P1 : P0) + g;
+          if (rq) {
+            float* d = (hq ? P0 : P1) + (int64_t)runq * P.stride + (int64_t)(S + q - bq);
 #pragma unroll
-          for (int a = 0; a < D; a++) xs[a] = src[a * RS];
-          float* d = (h ? P0 : P1) + dst;
-#pragma unroll
-          for (int a = 0; a < D; a++) d[a * RS] = xs[a];
+            for (int a = 0; a < D; a++) d[a * RS] = src[a * RS];
+          }
+          wvx[q] = src[3 * RS];
+          W.vy[q] = src[4 * RS];
+          W.vz[q] = src[5 * RS];
+          W.mod[q] = 0;
         }
-        s_vx[q] = vx;
-        s_vy[q] = vy;
-        s_vz[q] = vz;
-        s_mod[q] = 0;
       }
     }
-    __syncthreads();
-    // E: NTC.  E0: candidate counts M, block prefix, and a 16-bin counting
-    // sort of the cells by M (descending) so that each warp walks cells of
-    // similar M; then rounds of E1 (pair + direction draws of up to CCAP
-    // candidates, lane-parallel) and E2 (thread u walks the candidates of cell
-    // s_perm[u] in increasing k -- the sequential order of the method).
-    SmemCell A{s_vx + off, s_vy + off, s_vz + off, s_mod + off};
-    if (collide) {
+    __syncwarp();
+    // ---- E
+    if (mode == 0) {
       const uint32_t M = valid ? ntc_count(P, key, c, (uint32_t)s, N, gm) : 0u;
       ncand = M;
-      uint32_t tot;
-      const uint32_t mst = block_excl_scan(M, s_warp, tot);
-      s_mst[t] = mst;
-      if (t == CT - 1) s_mst[CT] = mst + M;
-      if (t < 16) s_bin[t] = 0;
-      __syncthreads();
-      const uint32_t bin = 15u - (M < 15u ? M : 15u);
-      const uint32_t slot_in_bin = atomicAdd(&s_bin[bin], 1u);
-      __syncthreads();
-      if (t < 32) {  // exclusive scan of the 16 bin counts
-        uint32_t v = t < 16 ? s_bin[t] : 0u, x = v;
+      uint32_t mst = M;
 #pragma unroll
-        for (int o = 1; o < 16; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, x, o); if ((t & 31) >= o) x += y; }
-        if (t < 16) s_bin[t] = x - v;
+      for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, mst, o); if (lane >= o) mst += y; }
+      const uint32_t tot = __shfl_sync(FULL, mst, 31);
+      mst -= M;                                   // exclusive prefix
+      // cells to lanes in descending M: bitonic sort of (M, lane) over the warp
+      uint32_t sk = ((M < 0xFFFFFFu ? M : 0xFFFFFFu) << 5) | (uint32_t)lane;
+#pragma unroll
+      for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+          const uint32_t o = __shfl_xor_sync(FULL, sk, j);
+          const bool up = ((lane & kk) == 0) != ((lane & j) == 0);   // keep the larger when true
+          sk = up ? max(sk, o) : min(sk, o);
+        }
       }
-      __syncthreads();
-      s_perm[s_bin[bin] + slot_in_bin] = (uint8_t)t;
-      __syncthreads();
-      // this thread's assigned cell
-      const int u = s_perm[t];
-      const uint32_t Mu = s_mst[u + 1] - s_mst[u], mstu = s_mst[u];
-      const uint32_t offu = s_st[u] - S;
-      const double gmu = (double)s_gm[u];
-      const double ghatu = gmu / P.sigma_c;
-      SmemCell Au{s_vx + offu, s_vy + offu, s_vz + offu, s_mod + offu};
+      const int u = (int)(sk & 31u);              // this lane walks cell u
+      const uint32_t Mu = __shfl_sync(FULL, M, u), mstu = __shfl_sync(FULL, mst, u);
+      const uint32_t offu = __shfl_sync(FULL, off, u);
+      const float gmuf = __shfl_sync(FULL, gm, u);
+      const double gmu = (double)gmuf, ghatu = gmu / P.sigma_c;
+      SmemCell Au{wvx + offu, W.vy + offu, W.vz + offu, W.mod + offu};
       float maxg2 = 0.0f;
       uint32_t naccu = 0;
-      for (uint32_t base = 0; base < tot; base += CCAP) {
-        const uint32_t lim = tot - base < (uint32_t)CCAP ? tot - base : (uint32_t)CCAP;
-        for (uint32_t q = t; q < lim; q += CT) {
+      for (uint32_t base = 0; base < tot; base += CCW) {
+        const uint32_t lim = tot - base < (uint32_t)CCW ? tot - base : (uint32_t)CCW;
+        for (uint32_t q0 = 0; q0 < lim; q0 += 32) {
+          const uint32_t q = q0 + lane;
           const uint32_t gq = base + q;
-          // cell of candidate gq: last cc with s_mst[cc] <= gq
-          int lo = 0, hi = CT;
-          while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (s_mst[mid] <= gq) lo = mid; else hi = mid; }
-          const int64_t kc = k0 + lo;
-          const int rc = r_first + s_ro[lo];
-          const uint32_t cc = (uint32_t)(kc - (int64_t)rc * P.Nc);
-          const uint32_t nc = s_n[lo];
-          const uint32_t kq = gq - s_mst[lo];
-          const uint2 keyc = run_key(P, rc);
-          const uint4 w = draw(keyc, cc, (uint32_t)s, TAG_COLL_PAIR, kq, 0);
-          const uint32_t i = lemire(w.x, nc);
-          uint32_t j = lemire(w.y, nc - 1);
-          if (j >= i) j++;
-          s_cij[q] = i | (j << 16);
-          s_cur[q] = w.z;
-          marsaglia_pq(keyc, cc, (uint32_t)s, kq, s_cp[q], s_cq[q]);
+          // owning cell of candidate gq: last lane with mst <= gq (binary search over lanes)
+          int lo = 0;
+#pragma unroll
+          for (int stp = 16; stp > 0; stp >>= 1) {
+            const uint32_t m = __shfl_sync(FULL, mst, lo + stp);
+            if (m <= gq && lo + stp < 32) lo += stp;
+          }
+          const uint32_t nc = __shfl_sync(FULL, N, lo), mlo = __shfl_sync(FULL, mst, lo);
+          const int rc = __shfl_sync(FULL, r, lo);
+          const uint32_t cc = __shfl_sync(FULL, c, lo);
+          if (q < lim) {
+            const uint32_t kq = gq - mlo;
+            const uint2 keyc = run_key(P, rc);
+            const uint4 w = draw(keyc, cc, (uint32_t)s, TAG_COLL_PAIR, kq, 0);
+            const uint32_t i = lemire(w.x, nc);
+            uint32_t j = lemire(w.y, nc - 1);
+            if (j >= i) j++;
+            W.cij[q] = i | (j << 16);
+            W.cur[q] = w.z;
+            marsaglia_pq(keyc, cc, (uint32_t)s, kq, W.cp[q], W.cq[q]);
+          }
         }
-        __syncthreads();
+        __syncwarp();
         if (Mu) {
           const uint32_t a0 = mstu > base ? mstu : base;
           const uint32_t a1 = mstu + Mu < base + lim ? mstu + Mu : base + lim;
           if (a0 < a1)
-            ntc_apply(P, Au, gmu, ghatu, s_cij + (a0 - base), s_cur + (a0 - base), s_cp + (a0 - base),
-                      s_cq + (a0 - base), a1 - a0, maxg2, naccu);
+            ntc_apply(P, Au, gmu, ghatu, W.cij + (a0 - base), W.cur + (a0 - base), W.cp + (a0 - base),
+                      W.cq + (a0 - base), a1 - a0, maxg2, naccu);
         }
-        __syncthreads();
+        __syncwarp();
       }
-      s_mg2[u] = maxg2;
-      s_nacc[u] = naccu;
-      __syncthreads();
+      W.mg2[u] = maxg2;
+      W.nacc[u] = naccu;
+      __syncwarp();
       if (valid && M) {
-        nacc = s_nacc[t];
-        const float mg = s_mg2[t];
+        nacc = W.nacc[lane];
+        const float mg = W.mg2[lane];
         const double sgm = P.model == 0 ? P.sigma_c * sqrt((double)mg) : P.sigma_c * pow((double)mg, P.omega1);
         if (sgm > (double)gm) gm = (float)sgm;
       }
     }
-    if (valid && slot >= 0) sample_cell(P, slot, k, N, A);
-    __syncthreads();
-    // F
+    if (valid && slot >= 0) sample_cell(P, slot, k, N, SmemCell{wvx + off, W.vy + off, W.vz + off, W.mod + off});
+    __syncwarp();
+    // ---- F
     if (one_run) {
-      const int h = s_h[0];
-      if (s_reo[0]) {
-        float* __restrict__ dx = (h ? P0 : P1) + 3 * RS + (int64_t)r_first * P.stride + (S - s_base[0]);
-        for (uint32_t q = t; q < cnt; q += CT) {
-          dx[q] = s_vx[q];
-          dx[RS + q] = s_vy[q];
-          dx[2 * RS + q] = s_vz[q];
+      if (reo) {
+        float* __restrict__ dx = (h ? P0 : P1) + 3 * RS + (int64_t)r * P.stride + (S - rbase);
+        for (uint32_t q = lane; q < cnt; q += 32) {
+          dx[q] = wvx[q];
+          dx[RS + q] = W.vy[q];
+          dx[2 * RS + q] = W.vz[q];
         }
       } else {
         float* __restrict__ vxp = (h ? P1 : P0) + 3 * RS;
-        for (uint32_t q = t; q < cnt; q += CT) {
-          if (s_mod[q]) {
-            const uint32_t g = s_sorted[q];
-            vxp[g] = s_vx[q];
-            vxp[RS + g] = s_vy[q];
-            vxp[2 * RS + g] = s_vz[q];
+        for (uint32_t q = lane; q < cnt; q += 32) {
+          if (W.mod[q]) {
+            const uint32_t g = W.sorted[q];
+            vxp[g] = wvx[q];
+            vxp[RS + g] = W.vy[q];
+            vxp[2 * RS + g] = W.vz[q];
           }
         }
       }
     } else {
-      for (uint32_t q = t; q < cnt; q += CT) {
-        const int ro = s_ro[s_cell[q]], h = s_h[ro];
-        if (s_reo[ro]) {
-          const int64_t dst = (int64_t)(r_first + ro) * P.stride + (int64_t)(S + q - s_base[ro]);
-          float* d = (h ? P0 : P1) + dst;
-          d[3 * RS] = s_vx[q];
-          d[4 * RS] = s_vy[q];
-          d[5 * RS] = s_vz[q];
-        } else if (s_mod[q]) {
-          float* d = (h ? P1 : P0) + s_sorted[q];
-          d[3 * RS] = s_vx[q];
-          d[4 * RS] = s_vy[q];
-          d[5 * RS] = s_vz[q];
+      for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        const int cq = q < cnt ? W.cell[q] : 0;
+        const int hq = __shfl_sync(FULL, h, cq), rq = __shfl_sync(FULL, reo, cq);
+        const int runq = __shfl_sync(FULL, r, cq);
+        const uint32_t bq = __shfl_sync(FULL, rbase, cq);
+        if (q < cnt) {
+          if (rq) {
+            float* d = (hq ? P0 : P1) + (int64_t)runq * P.stride + (int64_t)(S + q - bq);
+            d[3 * RS] = wvx[q];
+            d[4 * RS] = W.vy[q];
+            d[5 * RS] = W.vz[q];
+          } else if (W.mod[q]) {
+            float* d = (hq ? P1 : P0) + W.sorted[q];
+            d[3 * RS] = wvx[q];
+            d[4 * RS] = W.vy[q];
+            d[5 * RS] = W.vz[q];
+          }
         }
       }
     }
     if (P.debug)
-      for (uint32_t q = t; q < cnt; q += CT) P.lcr[S + q] = s_sorted[q];
+      for (uint32_t q = lane; q < cnt; q += 32) P.lcr[S + q] = W.sorted[q];
   } else if (valid) {
-    // tile too large for shared memory: this thread works on its own cell
-    // directly in global memory (segment sorted in place in LCR)
+    // tile too large for the warp's shared memory: each lane works on its
+    // own cell in global memory (segment sorted in place in LCR)
     uint32_t* seg = P.lcr + st;
     if (N <= 32) insertion_sort(seg, N);
     else heap_sort(seg, N);
-    const int ro = r - r_first;
-    const int h = s_h[ro];
     GlobCell A{seg, parr(P, h, 3), parr(P, h, 4), parr(P, h, 5)};
-    if (collide) collide_cell(P, key, c, (uint32_t)s, N, A, gm, ncand, nacc);
+    if (mode == 0) collide_cell(P, key, c, (uint32_t)s, N, A, gm, ncand, nacc);
     if (slot >= 0) sample_cell(P, slot, k, N, A);
-    if (s_reo[ro]) {
-      const uint32_t rb = s_base[ro];
+    if (reo) {
       for (uint32_t i = 0; i < N; i++) {
         const uint32_t g = seg[i];
-        const int64_t dst = (int64_t)r * P.stride + (int64_t)(st + i - rb);
+        const int64_t dst = (int64_t)r * P.stride + (int64_t)(st + i - rbase);
 #pragma unroll
         for (int a = 0; a < D; a++) parr(P, h ^ 1, a)[dst] = parr(P, h, a)[g];
 #pragma unroll
@@ -1119,7 +1133,7 @@ __global__ void __launch_bounds__(CT, 5) k_collide(Prm P, int mode, int slot_arg
     const uint32_t rk = valid ? (uint32_t)r : 0xFFFFFFFFu;
     const unsigned m = __match_any_sync(FULL, rk);
     const uint32_t sc = __reduce_add_sync(m, ncand), sa = __reduce_add_sync(m, nacc);
-    if (valid && (t & 31) == __ffs(m) - 1 && sc) {
+    if (valid && lane == __ffs(m) - 1 && sc) {
       atomicAdd(&P.ctl.counters[r * 4 + 2], (unsigned long long)sc);
       atomicAdd(&P.ctl.counters[r * 4 + 3], (unsigned long long)sa);
     }
@@ -1289,17 +1303,30 @@ void launch_step_mid(const Prm& P, cudaStream_t st) {
   k_step_mid<<<(P.R + 127) / 128, 128, 0, st>>>(P);
 }
 
-void launch_collide(const Prm& P, int mode, int slot, cudaStream_t st) {
+template <int D, int NET>
+static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t st) {
   const int64_t RN = (int64_t)P.R * P.Nc;
-  const unsigned g = (unsigned)((RN + CT - 1) / CT);
+  const int64_t warps = (RN + 31) / 32;
+  const unsigned g = (unsigned)((warps + WPB - 1) / WPB);
+  const size_t smem = WPB * warp_smem_bytes(capw);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(k_collide<D, NET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  k_collide<D, NET><<<g, WPB * 32, smem, st>>>(P, mode, slot, capw);
+}
+
+void launch_collide(const Prm& P, int mode, int slot, cudaStream_t st) {
   // register sorting network width: 16 for sparse cells, 32 for dense ones
   const bool wide = P.net_wide != 0;
+  const int capw = P.capw;
   if (P.dim == 1) {
-    if (wide) k_collide<1, 32><<<g, CT, 0, st>>>(P, mode, slot); else k_collide<1, 16><<<g, CT, 0, st>>>(P, mode, slot);
+    if (wide) collide_t<1, 32>(P, mode, slot, capw, st); else collide_t<1, 16>(P, mode, slot, capw, st);
   } else if (P.dim == 2) {
-    if (wide) k_collide<2, 32><<<g, CT, 0, st>>>(P, mode, slot); else k_collide<2, 16><<<g, CT, 0, st>>>(P, mode, slot);
+    if (wide) collide_t<2, 32>(P, mode, slot, capw, st); else collide_t<2, 16>(P, mode, slot, capw, st);
   } else {
-    if (wide) k_collide<3, 32><<<g, CT, 0, st>>>(P, mode, slot); else k_collide<3, 16><<<g, CT, 0, st>>>(P, mode, slot);
+    if (wide) collide_t<3, 32>(P, mode, slot, capw, st); else collide_t<3, 16>(P, mode, slot, capw, st);
   }
 }
 
