@@ -42,7 +42,7 @@ struct Layout {
   int64_t Nc, stride, RN;
   int32_t n_face;
   // ctl offsets
-  size_t c_step, c_status, c_nstore, c_parity, c_reorder, c_inserted, c_counters, c_live, c_psteps, c_slot;
+  size_t c_step, c_status, c_nstore, c_parity, c_reorder, c_inserted, c_counters, c_live, c_psteps, c_slot, c_queue;
   // scratch offsets
   size_t s_face_j, s_face_k, s_open, s_kept, s_part, s_macros, s_cand, s_acc;
 };
@@ -147,6 +147,7 @@ int make_layout(const dsmc_problem* p, int debug, Layout& L) {
   L.c_live = o; o = align_up(o + 8 * R, 16);
   L.c_psteps = o; o = align_up(o + 8 * R, 16);
   L.c_slot = o; o = align_up(o + 4 * (size_t)(s.n_slots > 0 ? s.n_slots : 1), 16);
+  L.c_queue = o; o = align_up(o + 8 * 8, 16);
   s.ctl = o;
   const size_t F = (size_t)p->ny * p->nz;
   o = 0;
@@ -325,6 +326,7 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   P.ctl.live = (int64_t*)(ct + L.c_live);
   P.ctl.psteps = (unsigned long long*)(ct + L.c_psteps);
   P.ctl.slot_done = (int32_t*)(ct + L.c_slot);
+  P.ctl.queue = (unsigned long long*)(ct + L.c_queue);
 
   auto bail = [&](int code) { delete c; return code; };
   std::vector<int32_t> fj, fk;

@@ -35,6 +35,7 @@ struct Ctl {
   int64_t* live;             // [R] live particles (after the last Indexing)
   unsigned long long* psteps;    // [R] sum over steps of live particles after Generation
   int32_t* slot_done;        // [n_slots]
+  unsigned long long* queue; // [4][2] work-queue cursors (item, blocks done) per persistent kernel
 };
 
 struct Prm {

@@ -420,6 +420,22 @@ __device__ __forceinline__ bool move_one(const Prm& P, uint2 key, uint32_t idx, 
   return false;
 }
 
+// Dynamic work queue for the persistent particle kernels: blocks take items
+// (ITEM consecutive particles of one run, run-major) from a global cursor, so
+// the items in flight stay within a window of ~one run and the cell counters
+// / LCR segments they hit stay resident in L2.  The last block to finish
+// resets the cursor for the next launch.
+constexpr int ITEM = 4096;
+__device__ __forceinline__ int64_t queue_next(unsigned long long* q, int64_t* s_item) {
+  __syncthreads();
+  if (threadIdx.x == 0) *s_item = (int64_t)atomicAdd(q, 1ull);
+  __syncthreads();
+  return *s_item;
+}
+__device__ __forceinline__ void queue_done(unsigned long long* q) {
+  if (threadIdx.x == 0 && atomicAdd(q + 1, 1ull) == gridDim.x - 1) { q[0] = 0; q[1] = 0; }
+}
+
 // Enumeration (reading R11): floor per axis, clamped.
 template <int D>
 __device__ __forceinline__ uint32_t enumerate(const Prm& P, const float x[3], const float v[3], uint32_t kbase) {
@@ -444,13 +460,14 @@ template <int D, bool EV>
 __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
   const int lane = threadIdx.x & 31;
   const uint32_t s = (uint32_t)*P.ctl.step;
-  const int64_t items_per_run = (P.cap + 1023) / 1024;
+  const int64_t items_per_run = (P.cap + ITEM - 1) / ITEM;
   const int64_t n_items = items_per_run * P.R;
-  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+  __shared__ int64_t s_item;
+  for (int64_t item = queue_next(P.ctl.queue, &s_item); item < n_items; item = queue_next(P.ctl.queue, &s_item)) {
   const int r = (int)(item / items_per_run);
   const int64_t n = P.ctl.n_store[r];
-  const int64_t i0w = (item - (int64_t)r * items_per_run) * 1024 + (threadIdx.x >> 5) * 128;
-  if (i0w - (threadIdx.x >> 5) * 128 >= n) continue;
+  const int64_t ibase = (item - (int64_t)r * items_per_run) * ITEM;
+  if (ibase >= n) continue;
   const int h = P.ctl.parity[r];
   const int64_t base = (int64_t)r * P.stride;
   float* X[3];
@@ -461,7 +478,7 @@ __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
   const uint2 key = run_key(P, r);
   const uint32_t kbase = (uint32_t)r * (uint32_t)P.Nc;
   uint32_t removed = 0;
-  {
+  for (int64_t i0w = ibase + (threadIdx.x >> 5) * 128; i0w < ibase + ITEM && i0w < n; i0w += 1024) {
     float x[4][3], v[4][3];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
@@ -513,6 +530,7 @@ __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
   for (int o = 16; o > 0; o >>= 1) removed += __shfl_xor_sync(FULL, removed, o);
   if (lane == 0 && removed) atomicAdd(&P.ctl.counters[r * 4 + 1], (unsigned long long)removed);
   }
+  queue_done(P.ctl.queue);
 }
 
 // ================================================================ control
@@ -564,15 +582,18 @@ __global__ void k_step_end(Prm P, int mode, int slot) {
 __global__ void __launch_bounds__(256) k_scatter(Prm P) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const int64_t items_per_run = (P.cap + 1023) / 1024;
+  const int64_t items_per_run = (P.cap + ITEM - 1) / ITEM;
   const int64_t n_items = items_per_run * P.R;
-  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+  __shared__ int64_t s_item;
+  for (int64_t item = queue_next(P.ctl.queue + 2, &s_item); item < n_items;
+       item = queue_next(P.ctl.queue + 2, &s_item)) {
     const int r = (int)(item / items_per_run);
     const int64_t n = P.ctl.n_store[r];
-    const int64_t i0w = (item - (int64_t)r * items_per_run) * 1024 + (threadIdx.x >> 5) * 128;
-    if (i0w - (threadIdx.x >> 5) * 128 >= n) continue;
+    const int64_t ibase = (item - (int64_t)r * items_per_run) * ITEM;
+    if (ibase >= n) continue;
     const int64_t base = (int64_t)r * P.stride;
     const uint32_t* K = P.key + base;
+    for (int64_t i0w = ibase + (threadIdx.x >> 5) * 128; i0w < ibase + ITEM && i0w < n; i0w += 1024) {
     uint32_t kk[4], m[4], p0[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
@@ -591,7 +612,9 @@ __global__ void __launch_bounds__(256) k_scatter(Prm P) {
       const uint32_t b = __shfl_sync(FULL, p0[j], __ffs(m[j]) - 1);
       if (kk[j] != DEAD_KEY) P.lcr[b + __popc(m[j] & lt)] = (uint32_t)(base + i0w + j * 32 + lane);
     }
+    }
   }
+  queue_done(P.ctl.queue + 2);
 }
 
 // ============================================================= Interaction
@@ -1258,7 +1281,7 @@ static void motion_t(const Prm& P, int mode, cudaStream_t st) {
   }
   // persistent: one wave of resident blocks walks the (run-major) items, so
   // the cell counters being hit at any moment belong to one or two runs
-  const int64_t items = (P.cap + 1023) / 1024 * P.R;
+  const int64_t items = (P.cap + ITEM - 1) / ITEM * P.R;
   int64_t g = (int64_t)num_sms() * occ;
   if (g > items) g = items;
   k_motion<D, EV><<<(unsigned)g, 256, 0, st>>>(P, mode);
@@ -1282,7 +1305,7 @@ void launch_scatter(const Prm& P, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter, 256, 0);
     if (occ < 1) occ = 1;
   }
-  const int64_t items = (P.cap + 1023) / 1024 * P.R;
+  const int64_t items = (P.cap + ITEM - 1) / ITEM * P.R;
   int64_t g = (int64_t)num_sms() * occ;
   if (g > items) g = items;
   k_scatter<<<(unsigned)g, 256, 0, st>>>(P);
