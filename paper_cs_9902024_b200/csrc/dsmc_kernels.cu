@@ -718,6 +718,24 @@ __device__ __forceinline__ uint32_t ntc_count(const Prm& P, uint2 key, uint32_t 
   return (uint32_t)M;
 }
 
+// Marsaglia pair from block b0 on (the first block is handled inline by k_collide)
+__device__ __noinline__ void marsaglia_pq_from(uint2 key, uint32_t c, uint32_t s, uint32_t k, uint32_t b0,
+                                               float& pp_out, float& qq_out) {
+  for (uint32_t blk = b0; blk < 64; blk++) {
+    const uint4 w = draw(key, c, s, TAG_COLL_DIR, k, blk);
+    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const float pp = 2.0f * u_co(ww[2 * h]) - 1.0f;
+      const float qq = 2.0f * u_co(ww[2 * h + 1]) - 1.0f;
+      const float rho = pp * pp + qq * qq;
+      if (rho < 1.0f) { pp_out = pp; qq_out = qq; return; }
+    }
+  }
+  pp_out = 0.0f;   // never reached in practice; gives e = (0, 0, 1) like marsaglia()
+  qq_out = 0.0f;
+}
+
 // the Marsaglia pair (p, q) of candidate k (reading R14), drawn ahead of use
 __device__ __forceinline__ void marsaglia_pq(uint2 key, uint32_t c, uint32_t s, uint32_t k, float& pp_out,
                                              float& qq_out) {
@@ -1017,50 +1035,60 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
       for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, mst, o); if (lane >= o) mst += y; }
       const uint32_t tot = __shfl_sync(FULL, mst, 31);
       mst -= M;                                   // exclusive prefix
-      // cells to lanes in descending M: bitonic sort of (M, lane) over the warp
-      uint32_t sk = ((M < 0xFFFFFFu ? M : 0xFFFFFFu) << 5) | (uint32_t)lane;
-#pragma unroll
-      for (int kk = 2; kk <= 32; kk <<= 1) {
-#pragma unroll
-        for (int j = kk >> 1; j > 0; j >>= 1) {
-          const uint32_t o = __shfl_xor_sync(FULL, sk, j);
-          const bool up = ((lane & kk) == 0) != ((lane & j) == 0);   // keep the larger when true
-          sk = up ? max(sk, o) : min(sk, o);
-        }
-      }
-      const int u = (int)(sk & 31u);              // this lane walks cell u
-      const uint32_t Mu = __shfl_sync(FULL, M, u), mstu = __shfl_sync(FULL, mst, u);
-      const uint32_t offu = __shfl_sync(FULL, off, u);
-      const float gmuf = __shfl_sync(FULL, gm, u);
-      const double gmu = (double)gmuf, ghatu = gmu / P.sigma_c;
-      SmemCell Au{wvx + offu, W.vy + offu, W.vz + offu, W.mod + offu};
+      const uint32_t Mu = M, mstu = mst;
+      const double gmu = (double)gm, ghatu = gmu / P.sigma_c;
+      SmemCell Au{wvx + off, W.vy + off, W.vz + off, W.mod + off};
       float maxg2 = 0.0f;
       uint32_t naccu = 0;
       for (uint32_t base = 0; base < tot; base += CCW) {
         const uint32_t lim = tot - base < (uint32_t)CCW ? tot - base : (uint32_t)CCW;
-        for (uint32_t q0 = 0; q0 < lim; q0 += 32) {
-          const uint32_t q = q0 + lane;
-          const uint32_t gq = base + q;
-          // owning cell of candidate gq: last lane with mst <= gq (binary search over lanes)
-          int lo = 0;
+        // two candidates per lane per pass: four independent Philox chains in flight
+        for (uint32_t q0 = 0; q0 < lim; q0 += 64) {
+          uint32_t qq[2], kq[2], nc[2], cc[2];
+          int rc[2];
 #pragma unroll
-          for (int stp = 16; stp > 0; stp >>= 1) {
-            const uint32_t m = __shfl_sync(FULL, mst, lo + stp);
-            if (m <= gq && lo + stp < 32) lo += stp;
+          for (int hh = 0; hh < 2; hh++) {
+            qq[hh] = q0 + 32 * hh + lane;
+            const uint32_t gq = base + qq[hh];
+            // owning cell of candidate gq: last lane with mst <= gq (binary search over lanes)
+            int lo = 0;
+#pragma unroll
+            for (int stp = 16; stp > 0; stp >>= 1) {
+              const uint32_t m = __shfl_sync(FULL, mst, lo + stp);
+              if (m <= gq && lo + stp < 32) lo += stp;
+            }
+            nc[hh] = __shfl_sync(FULL, N, lo);
+            kq[hh] = gq - __shfl_sync(FULL, mst, lo);
+            rc[hh] = __shfl_sync(FULL, r, lo);
+            cc[hh] = __shfl_sync(FULL, c, lo);
           }
-          const uint32_t nc = __shfl_sync(FULL, N, lo), mlo = __shfl_sync(FULL, mst, lo);
-          const int rc = __shfl_sync(FULL, r, lo);
-          const uint32_t cc = __shfl_sync(FULL, c, lo);
-          if (q < lim) {
-            const uint32_t kq = gq - mlo;
-            const uint2 keyc = run_key(P, rc);
-            const uint4 w = draw(keyc, cc, (uint32_t)s, TAG_COLL_PAIR, kq, 0);
-            const uint32_t i = lemire(w.x, nc);
-            uint32_t j = lemire(w.y, nc - 1);
-            if (j >= i) j++;
-            W.cij[q] = i | (j << 16);
-            W.cur[q] = w.z;
-            marsaglia_pq(keyc, cc, (uint32_t)s, kq, W.cp[q], W.cq[q]);
+          uint4 wp[2], wd[2];
+#pragma unroll
+          for (int hh = 0; hh < 2; hh++) {
+            const uint2 keyc = run_key(P, rc[hh]);
+            wp[hh] = draw(keyc, cc[hh], (uint32_t)s, TAG_COLL_PAIR, kq[hh], 0);
+            wd[hh] = draw(keyc, cc[hh], (uint32_t)s, TAG_COLL_DIR, kq[hh], 0);
+          }
+#pragma unroll
+          for (int hh = 0; hh < 2; hh++) {
+            const uint32_t q = qq[hh];
+            if (q < lim) {
+              const uint32_t i = lemire(wp[hh].x, nc[hh]);
+              uint32_t j = lemire(wp[hh].y, nc[hh] - 1);
+              if (j >= i) j++;
+              W.cij[q] = i | (j << 16);
+              W.cur[q] = wp[hh].z;
+              // Marsaglia pair: first block drawn above, further blocks only if both tries fail
+              float pp = 2.0f * u_co(wd[hh].x) - 1.0f, qv = 2.0f * u_co(wd[hh].y) - 1.0f;
+              if (!(pp * pp + qv * qv < 1.0f)) {
+                pp = 2.0f * u_co(wd[hh].z) - 1.0f;
+                qv = 2.0f * u_co(wd[hh].w) - 1.0f;
+                if (!(pp * pp + qv * qv < 1.0f))
+                  marsaglia_pq_from(run_key(P, rc[hh]), cc[hh], (uint32_t)s, kq[hh], 1, pp, qv);
+              }
+              W.cp[q] = pp;
+              W.cq[q] = qv;
+            }
           }
         }
         __syncwarp();
@@ -1073,13 +1101,9 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
         }
         __syncwarp();
       }
-      W.mg2[u] = maxg2;
-      W.nacc[u] = naccu;
-      __syncwarp();
       if (valid && M) {
-        nacc = W.nacc[lane];
-        const float mg = W.mg2[lane];
-        const double sgm = P.model == 0 ? P.sigma_c * sqrt((double)mg) : P.sigma_c * pow((double)mg, P.omega1);
+        nacc = naccu;
+        const double sgm = P.model == 0 ? P.sigma_c * sqrt((double)maxg2) : P.sigma_c * pow((double)maxg2, P.omega1);
         if (sgm > (double)gm) gm = (float)sgm;
       }
     }
