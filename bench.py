@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--timed-steps", type=int, default=4, help="steps of the per-kernel event-timed pass")
+    ap.add_argument("--reorder-every", type=int, default=None, help="physical reorder period K (problem parameter)")
     return ap.parse_args()
 
 
@@ -55,6 +56,8 @@ def workload(args, rank):
         kw = dict(n_runs=args.n_runs)
     p = configs.get(args.config, **kw)
     p["run_id0"] = rank * p["n_runs"]
+    if args.reorder_every is not None:
+        p["reorder_every"] = args.reorder_every
     return p
 
 
