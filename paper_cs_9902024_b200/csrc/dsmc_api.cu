@@ -283,10 +283,9 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
     int32_t ppc_max = 0;
     for (int k = 0; k < p->n_fill; k++) ppc_max = p->fill[k].ppc > ppc_max ? p->fill[k].ppc : ppc_max;
     if (p->inflow_kind == DSMC_INFLOW_GHOST) ppc_max = std::max(ppc_max, (int32_t)std::ceil(p->inflow_n));
-    // (mean + 5 sigma of a Poisson tile; overflowing tiles are rare and correct)
-    int32_t capw = 32 * ppc_max + 5 * (int32_t)std::ceil(std::sqrt(32.0 * ppc_max)) + 16;
-    capw = std::max(192, std::min(capw, 4096));
-    P.capw = (capw + 15) / 16 * 16;
+    int32_t capw = 32 * ppc_max + 8 * (int32_t)std::ceil(std::sqrt(32.0 * ppc_max)) + 64;
+    capw = std::max(256, std::min(capw, 4096));
+    P.capw = (capw + 31) / 32 * 32;
   }
   P.n_fill = p->n_fill;
   for (int k = 0; k < p->n_fill; k++) {

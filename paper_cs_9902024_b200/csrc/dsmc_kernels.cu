@@ -873,7 +873,7 @@ __device__ void heap_sort(uint32_t* a, uint32_t n) {
 //   F  write modified velocities back (or the whole tile to its new rank)
 // mode 0: full step; mode 1: sample only into `slot_arg` (dsmc_sample).
 constexpr int WPB = 4;      // warps per block
-constexpr int CCW = 96;     // pre-drawn candidates per round per warp
+constexpr int CCW = 128;    // pre-drawn candidates per round per warp
 
 struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
   uint32_t* sorted; uint32_t* a; float* vy; float* vz; uint8_t* cell; uint8_t* mod;
@@ -902,7 +902,7 @@ __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
 }
 
 template <int D, int NET>
-__global__ void __launch_bounds__(WPB * 32, 6) k_collide(Prm P, int mode, int slot_arg, int capw) {
+__global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_arg, int capw) {
   extern __shared__ __align__(16) uint8_t dsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const WarpSmem W = warp_smem(dsm + (size_t)wid * warp_smem_bytes(capw), capw);
