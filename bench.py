@@ -48,7 +48,7 @@ def parse():
     return ap.parse_args()
 
 
-def workload(args, rank):
+def workload(args, rank=0):
     kw = {}
     if args.config == "c4":
         kw = dict(n_runs=args.n_runs or 256, n_steps=100)
@@ -144,13 +144,14 @@ def run_ours(args):
     import torch.distributed as dist
     from paper_cs_9902024_b200 import dsmc
 
+    from paper_cs_9902024_b200 import runs
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl")
-    p = workload(args, rank)
+    p = runs.shard(workload(args, 0), rank, world)   # weak scaling: n runs per GPU, ids offset
     sim = dsmc.Simulation(p, device=f"cuda:{local}")
     sim.generate()
     stream = sim.stream
@@ -176,15 +177,8 @@ def run_ours(args):
     psteps = sum(b["particle_steps"] - a["particle_steps"] for a, b in zip(st0, st1))
     accepted = sum(b["accepted"] - a["accepted"] for a, b in zip(st0, st1)) / K
     live_avg = psteps / K
-    ms_t = torch.tensor([ms, float(psteps)], dtype=torch.float64, device=f"cuda:{local}")
-    if world > 1:
-        t_max = ms_t[:1].clone()
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        tot = ms_t[1:].clone()
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-        ms_max, psteps_all = float(t_max[0]), float(tot[0])
-    else:
-        ms_max, psteps_all = ms, float(psteps)
+    ms_max = runs.max_over_ranks(ms)
+    psteps_all = runs.sum_over_ranks(float(psteps))
     value = psteps_all / (ms_max / 1e3)
     kps = sim.kernels_per_step()
 
@@ -251,11 +245,7 @@ def run_ours(args):
         t1 = time.perf_counter()
         _, sb = sim.status()
         ps_e2e = sum(b["particle_steps"] - a["particle_steps"] for a, b in zip(sa, sb))
-        e2e_val = ps_e2e / (t1 - t0)
-        if world > 1:
-            tt = torch.tensor([t1 - t0], dtype=torch.float64, device=f"cuda:{local}")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_val = ps_e2e * world / float(tt[0])
+        e2e_val = runs.sum_over_ranks(ps_e2e) / runs.max_over_ranks(t1 - t0)
         e2e = {"value": e2e_val, "unit": "particle-steps/s", "h2d_bytes_per_step": nbytes_h2d // K,
                "d2h_bytes_per_step": macros.nbytes // K,
                "what": "set_state(all runs, pinned host) + K graph steps + dsmc_sample + dsmc_read_macros"}

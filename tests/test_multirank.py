@@ -1,0 +1,84 @@
+"""World-size-2 gloo test of the multi-GPU host path (CPU only).
+
+Two ranks each own half of the runs (runs.shard), produce their per-run
+snapshot sums (here with the oracle, since there is no GPU), exchange them
+with runs.gather_run_sums, and rank 0 forms the ensemble.  It must equal the
+single-process ensemble over all runs bit for bit (same fold order, R18), and
+the job time / particle-step reductions must be max / sum over ranks.
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, out_path):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle
+    from paper_cs_9902024_b200 import runs
+    from workloads import configs
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    job = configs.get("c2_small", n_runs=4, n_steps=20)
+    mine = runs.shard(job, rank, world, runs_per_rank=2)
+    assert mine["run_id0"] == 2 * rank and mine["n_runs"] == 2
+    sums = []
+    for r in range(mine["run_id0"], mine["run_id0"] + mine["n_runs"]):
+        o = oracle.OracleRun(mine, r)
+        o.fill()
+        o.step(20)
+        sums.append(o.get_snap(0))
+    local = torch.from_numpy(np.array(sums).transpose(1, 0, 2).copy())   # [5][n_local][Nc]
+    full = runs.gather_run_sums(local)
+    t = runs.max_over_ranks(1.0 + rank)
+    n = runs.sum_over_ranks(10.0 * (rank + 1))
+    if rank == 0:
+        ens = oracle.ensemble(full.numpy().transpose(1, 0, 2), job["fnum_vc"])
+        np.savez(out_path, ens=ens, t=t, n=n)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_ensemble_equals_single(tmp_path, oracle_mod):
+    from workloads import configs
+    out = str(tmp_path / "r0.npz")
+    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = np.load(out)
+    assert got["t"] == 2.0 and got["n"] == 30.0
+    job = configs.get("c2_small", n_runs=4, n_steps=20)
+    sums = []
+    for r in range(4):
+        o = oracle_mod.OracleRun(job, r)
+        o.fill()
+        o.step(20)
+        sums.append(o.get_snap(0))
+    want = oracle_mod.ensemble(np.array(sums), job["fnum_vc"])
+    assert np.array_equal(np.nan_to_num(got["ens"], nan=-7.0), np.nan_to_num(want, nan=-7.0))
+
+
+def test_shard_offsets():
+    sys.path.insert(0, ROOT)
+    from paper_cs_9902024_b200 import runs
+    from workloads import configs
+    p = configs.get("c4_small", n_runs=3)
+    shards = [runs.shard(p, k, 4) for k in range(4)]
+    ids = [i for q in shards for i in range(q["run_id0"], q["run_id0"] + q["n_runs"])]
+    assert ids == list(range(12))
