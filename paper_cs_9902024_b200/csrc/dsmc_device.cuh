@@ -90,7 +90,6 @@ struct Prm {
   int32_t debug;
   int32_t net_wide;          // k_collide sorts segments of <= 32 (else 16) in registers
   int32_t capw;              // particles a warp tile (32 cells) stages in shared memory
-  int32_t pf_ahead;          // k_collide L2 prefetch distance in tiles (<0 disables)
   int64_t* dbg_cand;         // [R*Nc]
   int32_t* dbg_acc;          // [R*Nc]
   Ctl ctl;

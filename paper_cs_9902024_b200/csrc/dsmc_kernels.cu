@@ -901,19 +901,6 @@ __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
   return w;
 }
 
-// bulk L2 prefetch of a contiguous byte range (TMA engine; no registers held)
-__device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
-  uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
-  int64_t n = (int64_t)(reinterpret_cast<uintptr_t>(p) + bytes - a);
-  n = (n + 15) & ~(int64_t)15;
-  while (n > 0) {
-    const uint32_t chunk = n > (1 << 20) ? (1u << 20) : (uint32_t)n;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(chunk) : "memory");
-    a += chunk;
-    n -= chunk;
-  }
-}
-
 template <int D, int NET>
 __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_arg, int capw) {
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -949,28 +936,6 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
   const int h = P.ctl.parity[r];
   const int reo = mode == 0 ? P.ctl.reorder[r] : 0;
   const uint32_t rbase = run_lcr_base(P, r);
-  // L2 prefetch for the warp tile one resident wave ahead: its LCR slice and
-  // (the store being near-sorted) the matching velocity range of its run
-  if (P.pf_ahead > 0 && lane < 2) {
-    const int64_t kf = k0 + (int64_t)P.pf_ahead * 32;
-    if (kf + 32 <= RN) {
-      const uint32_t fs = kf == 0 ? 0u : P.cell[kf - 1], fe = P.cell[kf + 31];
-      if (fe > fs) {
-        if (lane == 0) {
-          prefetch_l2(P.lcr + fs, 4 * (int64_t)(fe - fs));
-        } else {
-          const int rf = (int)((uint32_t)kf / Nc32);
-          const uint32_t fb = run_lcr_base(P, rf);
-          const int hf = P.ctl.parity[rf];
-          const int64_t g0 = (int64_t)rf * P.stride + (int64_t)(fs - fb);
-          const float* vb = (hf ? P1 : P0) + 3 * RS + g0;
-          prefetch_l2(vb, 4 * (int64_t)(fe - fs));
-          prefetch_l2(vb + RS, 4 * (int64_t)(fe - fs));
-          prefetch_l2(vb + 2 * RS, 4 * (int64_t)(fe - fs));
-        }
-      }
-    }
-  }
   const int32_t s = *P.ctl.step;
   int slot = -1;
   if (mode == 0) {
@@ -1386,21 +1351,16 @@ void launch_step_mid(const Prm& P, cudaStream_t st) {
 }
 
 template <int D, int NET>
-static void collide_t(const Prm& P0_, int mode, int slot, int capw, cudaStream_t st) {
-  const int64_t RN = (int64_t)P0_.R * P0_.Nc;
+static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t st) {
+  const int64_t RN = (int64_t)P.R * P.Nc;
   const int64_t warps = (RN + 31) / 32;
   const unsigned g = (unsigned)((warps + WPB - 1) / WPB);
   const size_t smem = WPB * warp_smem_bytes(capw);
   static size_t configured = 0;
-  static int occ = 0;
   if (smem > configured) {
     cudaFuncSetAttribute(k_collide<D, NET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = smem;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collide<D, NET>, WPB * 32, smem);
-    if (occ < 1) occ = 1;
   }
-  Prm P = P0_;
-  P.pf_ahead = P.pf_ahead < 0 ? 0 : num_sms() * occ * WPB;   // tiles one resident wave ahead
   k_collide<D, NET><<<g, WPB * 32, smem, st>>>(P, mode, slot, capw);
 }
 
