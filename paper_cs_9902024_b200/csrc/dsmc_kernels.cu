@@ -948,8 +948,20 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
   float gm = valid ? P.gmax[k] : 0.0f;
   const float gm0 = gm;
   if (cnt <= (uint32_t)capw) {
-    // ---- B
-    for (uint32_t q = lane; q < cnt; q += 32) W.a[q] = P.lcr[S + q];
+    // ---- B (loads batched 8 deep per lane so their latencies overlap)
+    for (uint32_t q0 = 0; q0 < cnt; q0 += 256) {
+      uint32_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const uint32_t q = q0 + 32 * u + lane;
+        if (q < cnt) v[u] = P.lcr[S + q];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const uint32_t q = q0 + 32 * u + lane;
+        if (q < cnt) W.a[q] = v[u];
+      }
+    }
     if (valid) for (uint32_t i = 0; i < N; i++) W.cell[off + i] = (uint8_t)lane;
     __syncwarp();
     // ---- C
@@ -979,28 +991,66 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
     float* const wvx = reinterpret_cast<float*>(W.a);
     if (one_run) {
       const float* __restrict__ sx = (h ? P1 : P0) + 3 * RS;
+      // gathers batched per lane (4 or 8 elements' loads issued before any store)
       if (reo) {
         const float* __restrict__ px = (h ? P1 : P0);
         float* __restrict__ dx = (h ? P0 : P1) + (int64_t)r * P.stride + (S - rbase);
-        for (uint32_t q = lane; q < cnt; q += 32) {
-          const uint32_t g = W.sorted[q];
-          float xs[D];
+        for (uint32_t q0 = 0; q0 < cnt; q0 += 128) {
+          uint32_t gg[4];
+          float xs[4][D], vv[4][3];
 #pragma unroll
-          for (int a = 0; a < D; a++) xs[a] = px[a * RS + g];
-          wvx[q] = sx[g];
-          W.vy[q] = sx[RS + g];
-          W.vz[q] = sx[2 * RS + g];
-          W.mod[q] = 0;
+          for (int u = 0; u < 4; u++) {
+            const uint32_t q = q0 + 32 * u + lane;
+            gg[u] = q < cnt ? W.sorted[q] : 0u;
+          }
 #pragma unroll
-          for (int a = 0; a < D; a++) dx[a * RS + q] = xs[a];
+          for (int u = 0; u < 4; u++) {
+            if (q0 + 32 * u + lane < cnt) {
+#pragma unroll
+              for (int a = 0; a < D; a++) xs[u][a] = px[a * RS + gg[u]];
+#pragma unroll
+              for (int a = 0; a < 3; a++) vv[u][a] = sx[a * RS + gg[u]];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const uint32_t q = q0 + 32 * u + lane;
+            if (q < cnt) {
+              wvx[q] = vv[u][0];
+              W.vy[q] = vv[u][1];
+              W.vz[q] = vv[u][2];
+              W.mod[q] = 0;
+#pragma unroll
+              for (int a = 0; a < D; a++) dx[a * RS + q] = xs[u][a];
+            }
+          }
         }
       } else {
-        for (uint32_t q = lane; q < cnt; q += 32) {
-          const uint32_t g = W.sorted[q];
-          wvx[q] = sx[g];
-          W.vy[q] = sx[RS + g];
-          W.vz[q] = sx[2 * RS + g];
-          W.mod[q] = 0;
+        for (uint32_t q0 = 0; q0 < cnt; q0 += 256) {
+          uint32_t gg[8];
+          float vv[8][3];
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            const uint32_t q = q0 + 32 * u + lane;
+            gg[u] = q < cnt ? W.sorted[q] : 0u;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            if (q0 + 32 * u + lane < cnt) {
+#pragma unroll
+              for (int a = 0; a < 3; a++) vv[u][a] = sx[a * RS + gg[u]];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            const uint32_t q = q0 + 32 * u + lane;
+            if (q < cnt) {
+              wvx[q] = vv[u][0];
+              W.vy[q] = vv[u][1];
+              W.vz[q] = vv[u][2];
+              W.mod[q] = 0;
+            }
+          }
         }
       }
     } else {
