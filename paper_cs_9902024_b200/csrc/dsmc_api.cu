@@ -5,7 +5,6 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
-#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -284,13 +283,7 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
     int32_t ppc_max = 0;
     for (int k = 0; k < p->n_fill; k++) ppc_max = p->fill[k].ppc > ppc_max ? p->fill[k].ppc : ppc_max;
     if (p->inflow_kind == DSMC_INFLOW_GHOST) ppc_max = std::max(ppc_max, (int32_t)std::ceil(p->inflow_n));
-    // two cells per lane (64-cell warp tiles) balance the NTC work; dense
-    // fills keep one cell per lane so that a tile still fits
-    const char* env = std::getenv("DSMC_CPL");
-    P.cpl = env ? std::atoi(env) : (ppc_max <= 12 ? 2 : 1);
-    if (P.cpl != 1 && P.cpl != 2) P.cpl = 2;
-    const int32_t tc = 32 * P.cpl;
-    int32_t capw = tc * ppc_max + 8 * (int32_t)std::ceil(std::sqrt((double)tc * ppc_max)) + 64;
+    int32_t capw = 32 * ppc_max + 8 * (int32_t)std::ceil(std::sqrt(32.0 * ppc_max)) + 64;
     capw = std::max(256, std::min(capw, 4096));
     P.capw = (capw + 31) / 32 * 32;
   }

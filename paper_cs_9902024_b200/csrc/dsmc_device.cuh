@@ -89,8 +89,7 @@ struct Prm {
   double* macros;            // [Nc][10] staging
   int32_t debug;
   int32_t net_wide;          // k_collide sorts segments of <= 32 (else 16) in registers
-  int32_t capw;              // particles a warp tile stages in shared memory
-  int32_t cpl;               // cells per lane in k_collide (warp tile = 32*cpl cells)
+  int32_t capw;              // particles a warp tile (32 cells) stages in shared memory
   int64_t* dbg_cand;         // [R*Nc]
   int32_t* dbg_acc;          // [R*Nc]
   Ctl ctl;

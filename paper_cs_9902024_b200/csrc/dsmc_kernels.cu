@@ -854,29 +854,26 @@ __device__ void heap_sort(uint32_t* a, uint32_t n) {
 }
 
 // ---------------------------------------------------------------------------
-// k_collide: Interaction + Sampling (+ physical reorder) for warp tiles of
-// TC = 32*CPL consecutive (run, cell) keys.  Each WARP owns one tile
-// independently; lane l owns cells l + 32 j (j < CPL): per-cell scalars stay
-// in registers and are exchanged by shuffles, the tile's particles are staged
-// in the warp's slice of shared memory, and phases are separated by
-// __syncwarp only, so the warps of an SM overlap their memory and compute
-// phases freely.
+// k_collide: Interaction + Sampling (+ physical reorder) for tiles of 32
+// consecutive (run, cell) keys.  Each WARP owns one tile independently (lane
+// = cell): per-cell scalars stay in registers and are exchanged by shuffles,
+// the tile's particles are staged in the warp's slice of shared memory, and
+// phases are separated by __syncwarp only, so the warps of an SM overlap
+// their memory and compute phases freely.
 //   A  segment bounds from the LCR ends, run metadata
-//   B  stage the tile's LCR slice; tag each position with its cell
+//   B  stage the tile's LCR slice; tag each position with its cell (lane)
 //   C  canonical order (R11): lanes sort segments of <= NET in registers
 //      (bitonic network); bigger segments rank every element
 //   D  gather velocities in canonical order; on reorder steps copy positions
 //      to their canonical rank in the other half of P
-//   E  NTC: M per cell, tile prefix; with CPL = 2 the cells are ranked by M
-//      (bitonic over the warp) and lane l walks the cells of rank l and
-//      63 - l, which balances the lanes' sequential work.  Rounds of
-//      pre-drawn candidates (pair, acceptance word, Marsaglia pair) are
-//      computed lane-parallel; each lane then walks its cells' candidates in
-//      increasing k -- the method's sequential order
+//   E  NTC: M per cell, warp prefix, cells reassigned to lanes in order of M
+//      (bitonic over the warp); rounds of pre-drawn candidates (pair,
+//      acceptance word, Marsaglia pair), then each lane walks one cell's
+//      candidates in increasing k -- the method's sequential order
 //   F  write modified velocities back (or the whole tile to its new rank)
 // mode 0: full step; mode 1: sample only into `slot_arg` (dsmc_sample).
 constexpr int WPB = 4;      // warps per block
-constexpr int CCW = 192;    // pre-drawn candidates per round per warp
+constexpr int CCW = 128;    // pre-drawn candidates per round per warp
 
 struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
   uint32_t* sorted; uint32_t* a; float* vy; float* vz; uint8_t* cell; uint8_t* mod;
@@ -884,7 +881,7 @@ struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
 };
 
 __host__ __device__ inline size_t warp_smem_bytes(int capw) {
-  return (size_t)capw * 18 + (size_t)CCW * 16 + 64 * 8 + 16;
+  return (size_t)capw * 18 + (size_t)CCW * 16 + 32 * 8 + 16;
 }
 
 __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
@@ -898,27 +895,14 @@ __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
   w.cp = reinterpret_cast<float*>(w.cur + CCW);
   w.cq = w.cp + CCW;
   w.mg2 = w.cq + CCW;
-  w.nacc = reinterpret_cast<uint32_t*>(w.mg2 + 64);
-  w.cell = reinterpret_cast<uint8_t*>(w.nacc + 64);
+  w.nacc = reinterpret_cast<uint32_t*>(w.mg2 + 32);
+  w.cell = reinterpret_cast<uint8_t*>(w.nacc + 32);
   w.mod = w.cell + capw;
   return w;
 }
 
-// value of per-slot register v of tile cell cq (lane cq & 31, slot cq >> 5)
-template <int CPL, class T>
-__device__ __forceinline__ T cell_get(const T (&v)[CPL], int cq) {
-  T res = T();
-#pragma unroll
-  for (int j = 0; j < CPL; j++) {
-    const T t = __shfl_sync(FULL, v[j], cq & 31);
-    if ((cq >> 5) == j) res = t;
-  }
-  return res;
-}
-
-template <int D, int NET, int CPL>
+template <int D, int NET>
 __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_arg, int capw) {
-  constexpr int TC = 32 * CPL;
   extern __shared__ __align__(16) uint8_t dsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const WarpSmem W = warp_smem(dsm + (size_t)wid * warp_smem_bytes(capw), capw);
@@ -926,14 +910,32 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
   const int64_t RS = (int64_t)P.R * P.stride;
   float* const P0 = P.P;
   float* const P1 = P.P + P.half;
-  const int64_t k0 = ((int64_t)blockIdx.x * WPB + wid) * TC;
+  const int64_t k0 = ((int64_t)blockIdx.x * WPB + wid) * 32;
   if (k0 >= RN) return;                          // whole warp leaves together
-  const int64_t klast = k0 + TC - 1 < RN ? k0 + TC - 1 : RN - 1;
-  const int cl_last = (int)(klast - k0);
+  const int64_t k = k0 + lane;
+  const bool valid = k < RN;
+  const int64_t klast = k0 + 31 < RN ? k0 + 31 : RN - 1;
+  const int last_lane = (int)(klast - k0);
   const uint32_t Nc32 = (uint32_t)P.Nc;          // R*Nc < 2^31 (checked in dsmc_create)
   const int r_first = (int)((uint32_t)k0 / Nc32);
   const int r_last = (int)((uint32_t)klast / Nc32);
   const bool one_run = r_first == r_last;
+  // ---- A
+  uint32_t st = 0, en = 0;
+  if (valid) {
+    st = k == 0 ? 0u : P.cell[k - 1];
+    en = P.cell[k];
+  }
+  const int r = valid ? (int)((uint32_t)k / Nc32) : r_last;
+  const uint32_t c = valid ? (uint32_t)k - (uint32_t)r * Nc32 : 0u;
+  const uint32_t N = en - st;
+  const uint32_t S = __shfl_sync(FULL, st, 0);
+  const uint32_t E = __shfl_sync(FULL, en, last_lane);
+  const uint32_t cnt = E - S;
+  const uint32_t off = st - S;
+  const int h = P.ctl.parity[r];
+  const int reo = mode == 0 ? P.ctl.reorder[r] : 0;
+  const uint32_t rbase = run_lcr_base(P, r);
   const int32_t s = *P.ctl.step;
   int slot = -1;
   if (mode == 0) {
@@ -941,39 +943,10 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
   } else {
     slot = slot_arg;
   }
-  // ---- A
-  bool valid[CPL];
-  uint32_t st[CPL], N[CPL], off[CPL], c[CPL], rbase[CPL], ncand[CPL], nacc[CPL];
-  int r[CPL], h[CPL], reo[CPL];
-  float gm[CPL], gm0[CPL];
-  uint32_t en_last = 0;
-#pragma unroll
-  for (int j = 0; j < CPL; j++) {
-    const int64_t k = k0 + lane + 32 * j;
-    valid[j] = k < RN;
-    uint32_t e = 0;
-    st[j] = 0;
-    if (valid[j]) {
-      st[j] = k == 0 ? 0u : P.cell[k - 1];
-      e = P.cell[k];
-    }
-    if ((cl_last >> 5) == j) en_last = e;
-    N[j] = e - st[j];
-    r[j] = valid[j] ? (int)((uint32_t)k / Nc32) : r_last;
-    c[j] = valid[j] ? (uint32_t)k - (uint32_t)r[j] * Nc32 : 0u;
-    h[j] = P.ctl.parity[r[j]];
-    reo[j] = mode == 0 ? P.ctl.reorder[r[j]] : 0;
-    rbase[j] = run_lcr_base(P, r[j]);
-    gm[j] = valid[j] ? P.gmax[k] : 0.0f;
-    gm0[j] = gm[j];
-    ncand[j] = 0;
-    nacc[j] = 0;
-  }
-  const uint32_t S = __shfl_sync(FULL, st[0], 0);
-  const uint32_t E = __shfl_sync(FULL, en_last, cl_last & 31);
-  const uint32_t cnt = E - S;
-#pragma unroll
-  for (int j = 0; j < CPL; j++) off[j] = st[j] - S;
+  const uint2 key = run_key(P, r);
+  uint32_t ncand = 0, nacc = 0;
+  float gm = valid ? P.gmax[k] : 0.0f;
+  const float gm0 = gm;
   if (cnt <= (uint32_t)capw) {
     // ---- B (loads batched 8 deep per lane so their latencies overlap)
     for (uint32_t q0 = 0; q0 < cnt; q0 += 256) {
@@ -989,29 +962,22 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
         if (q < cnt) W.a[q] = v[u];
       }
     }
-#pragma unroll
-    for (int j = 0; j < CPL; j++)
-      if (valid[j]) for (uint32_t i = 0; i < N[j]; i++) W.cell[off[j] + i] = (uint8_t)(lane + 32 * j);
+    if (valid) for (uint32_t i = 0; i < N; i++) W.cell[off + i] = (uint8_t)lane;
     __syncwarp();
     // ---- C
-    bool big = false;
+    if (valid && N <= (uint32_t)NET) {
+      uint32_t v[NET];
 #pragma unroll
-    for (int j = 0; j < CPL; j++) {
-      big = big || (valid[j] && N[j] > (uint32_t)NET);
-      if (valid[j] && N[j] <= (uint32_t)NET) {
-        uint32_t v[NET];
+      for (int i = 0; i < NET; i++) v[i] = (uint32_t)i < N ? W.a[off + i] : 0xFFFFFFFFu;
+      sort_net<NET>(v);
 #pragma unroll
-        for (int i = 0; i < NET; i++) v[i] = (uint32_t)i < N[j] ? W.a[off[j] + i] : 0xFFFFFFFFu;
-        sort_net<NET>(v);
-#pragma unroll
-        for (int i = 0; i < NET; i++) if ((uint32_t)i < N[j]) W.sorted[off[j] + i] = v[i];
-      }
+      for (int i = 0; i < NET; i++) if ((uint32_t)i < N) W.sorted[off + i] = v[i];
     }
-    if (__any_sync(FULL, big)) {
+    if (__any_sync(FULL, valid && N > (uint32_t)NET)) {
       for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
         const uint32_t q = q0 + lane;
         const int cq = q < cnt ? W.cell[q] : 0;
-        const uint32_t n = cell_get<CPL>(N, cq), b = cell_get<CPL>(off, cq);
+        const uint32_t n = __shfl_sync(FULL, N, cq), b = __shfl_sync(FULL, off, cq);
         if (q < cnt && n > (uint32_t)NET) {
           const uint32_t v = W.a[q];
           uint32_t rank = 0;
@@ -1024,12 +990,11 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
     // ---- D
     float* const wvx = reinterpret_cast<float*>(W.a);
     if (one_run) {
-      const int hh = h[0];
-      const float* __restrict__ sx = (hh ? P1 : P0) + 3 * RS;
+      const float* __restrict__ sx = (h ? P1 : P0) + 3 * RS;
       // gathers batched per lane (4 or 8 elements' loads issued before any store)
-      if (reo[0]) {
-        const float* __restrict__ px = (hh ? P1 : P0);
-        float* __restrict__ dx = (hh ? P0 : P1) + (int64_t)r[0] * P.stride + (S - rbase[0]);
+      if (reo) {
+        const float* __restrict__ px = (h ? P1 : P0);
+        float* __restrict__ dx = (h ? P0 : P1) + (int64_t)r * P.stride + (S - rbase);
         for (uint32_t q0 = 0; q0 < cnt; q0 += 128) {
           uint32_t gg[4];
           float xs[4][D], vv[4][3];
@@ -1092,8 +1057,9 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
       for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
         const uint32_t q = q0 + lane;
         const int cq = q < cnt ? W.cell[q] : 0;
-        const int hq = cell_get<CPL>(h, cq), rq = cell_get<CPL>(reo, cq), runq = cell_get<CPL>(r, cq);
-        const uint32_t bq = cell_get<CPL>(rbase, cq);
+        const int hq = __shfl_sync(FULL, h, cq), rq = __shfl_sync(FULL, reo, cq);
+        const int runq = __shfl_sync(FULL, r, cq);
+        const uint32_t bq = __shfl_sync(FULL, rbase, cq);
         if (q < cnt) {
           const uint32_t g = W.sorted[q];
           const float* src = (hq ? P1 : P0) + g;
@@ -1112,62 +1078,18 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
     __syncwarp();
     // ---- E
     if (mode == 0) {
-      uint32_t M[CPL], mst[CPL], tot = 0;
+      const uint32_t M = valid ? ntc_count(P, key, c, (uint32_t)s, N, gm) : 0u;
+      ncand = M;
+      uint32_t mst = M;
 #pragma unroll
-      for (int j = 0; j < CPL; j++) {
-        M[j] = valid[j] ? ntc_count(P, run_key(P, r[j]), c[j], (uint32_t)s, N[j], gm[j]) : 0u;
-        ncand[j] = M[j];
-        uint32_t x = M[j];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, x, o); if (lane >= o) x += y; }
-        mst[j] = tot + x - M[j];
-        tot += __shfl_sync(FULL, x, 31);
-      }
-      // cells this lane walks: with CPL = 2, ranks l and 63 - l of M
-      int u[CPL];
-      if (CPL == 2) {
-        uint32_t key[CPL];
-#pragma unroll
-        for (int j = 0; j < CPL; j++) key[j] = ((M[j] < 0x3FFFFFFu ? M[j] : 0x3FFFFFFu) << 6) | (uint32_t)(lane + 32 * j);
-#pragma unroll
-        for (int kk = 2; kk <= TC; kk <<= 1) {
-#pragma unroll
-          for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-            if (jj == 32) {
-              const uint32_t lo = min(key[0], key[CPL - 1]), hi = max(key[0], key[CPL - 1]);
-              key[0] = lo;
-              key[CPL - 1] = hi;
-            } else {
-#pragma unroll
-              for (int j = 0; j < CPL; j++) {
-                const int e = lane + 32 * j;
-                const uint32_t o = __shfl_xor_sync(FULL, key[j], jj);
-                const bool asc = (e & kk) == 0;
-                const bool keep_min = ((e & jj) == 0) == asc;
-                key[j] = keep_min ? min(key[j], o) : max(key[j], o);
-              }
-            }
-          }
-        }
-        u[0] = (int)(key[0] & 63u);
-        u[CPL - 1] = (int)(__shfl_sync(FULL, key[CPL - 1], 31 - lane) & 63u);
-      } else {
-#pragma unroll
-        for (int j = 0; j < CPL; j++) u[j] = lane + 32 * j;
-      }
-      uint32_t Mu[CPL], mstu[CPL], offu[CPL], naccu[CPL];
-      double gmu[CPL], ghatu[CPL];
-      float maxg2[CPL];
-#pragma unroll
-      for (int j = 0; j < CPL; j++) {
-        Mu[j] = cell_get<CPL>(M, u[j]);
-        mstu[j] = cell_get<CPL>(mst, u[j]);
-        offu[j] = cell_get<CPL>(off, u[j]);
-        gmu[j] = (double)cell_get<CPL>(gm, u[j]);
-        ghatu[j] = gmu[j] / P.sigma_c;
-        maxg2[j] = 0.0f;
-        naccu[j] = 0;
-      }
+      for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, mst, o); if (lane >= o) mst += y; }
+      const uint32_t tot = __shfl_sync(FULL, mst, 31);
+      mst -= M;                                   // exclusive prefix
+      const uint32_t Mu = M, mstu = mst;
+      const double gmu = (double)gm, ghatu = gmu / P.sigma_c;
+      SmemCell Au{wvx + off, W.vy + off, W.vz + off, W.mod + off};
+      float maxg2 = 0.0f;
+      uint32_t naccu = 0;
       for (uint32_t base = 0; base < tot; base += CCW) {
         const uint32_t lim = tot - base < (uint32_t)CCW ? tot - base : (uint32_t)CCW;
         // two candidates per lane per pass: four independent Philox chains in flight
@@ -1178,17 +1100,17 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
           for (int hh = 0; hh < 2; hh++) {
             qq[hh] = q0 + 32 * hh + lane;
             const uint32_t gq = base + qq[hh];
-            // owning cell of candidate gq: last tile cell with mst <= gq
+            // owning cell of candidate gq: last lane with mst <= gq (binary search over lanes)
             int lo = 0;
 #pragma unroll
-            for (int stp = TC / 2; stp > 0; stp >>= 1) {
-              const uint32_t m = cell_get<CPL>(mst, (lo + stp) & (TC - 1));
-              if (lo + stp < TC && m <= gq) lo += stp;
+            for (int stp = 16; stp > 0; stp >>= 1) {
+              const uint32_t m = __shfl_sync(FULL, mst, lo + stp);
+              if (m <= gq && lo + stp < 32) lo += stp;
             }
-            nc[hh] = cell_get<CPL>(N, lo);
-            kq[hh] = gq - cell_get<CPL>(mst, lo);
-            rc[hh] = cell_get<CPL>(r, lo);
-            cc[hh] = cell_get<CPL>(c, lo);
+            nc[hh] = __shfl_sync(FULL, N, lo);
+            kq[hh] = gq - __shfl_sync(FULL, mst, lo);
+            rc[hh] = __shfl_sync(FULL, r, lo);
+            cc[hh] = __shfl_sync(FULL, c, lo);
           }
           uint4 wp[2], wd[2];
 #pragma unroll
@@ -1202,9 +1124,9 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
             const uint32_t q = qq[hh];
             if (q < lim) {
               const uint32_t i = lemire(wp[hh].x, nc[hh]);
-              uint32_t jx = lemire(wp[hh].y, nc[hh] - 1);
-              if (jx >= i) jx++;
-              W.cij[q] = i | (jx << 16);
+              uint32_t j = lemire(wp[hh].y, nc[hh] - 1);
+              if (j >= i) j++;
+              W.cij[q] = i | (j << 16);
               W.cur[q] = wp[hh].z;
               // Marsaglia pair: first block drawn above, further blocks only if both tries fail
               float pp = 2.0f * u_co(wd[hh].x) - 1.0f, qv = 2.0f * u_co(wd[hh].y) - 1.0f;
@@ -1220,59 +1142,34 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
           }
         }
         __syncwarp();
-#pragma unroll
-        for (int j = 0; j < CPL; j++) {
-          if (Mu[j]) {
-            const uint32_t a0 = mstu[j] > base ? mstu[j] : base;
-            const uint32_t a1 = mstu[j] + Mu[j] < base + lim ? mstu[j] + Mu[j] : base + lim;
-            if (a0 < a1) {
-              SmemCell Au{wvx + offu[j], W.vy + offu[j], W.vz + offu[j], W.mod + offu[j]};
-              ntc_apply(P, Au, gmu[j], ghatu[j], W.cij + (a0 - base), W.cur + (a0 - base), W.cp + (a0 - base),
-                        W.cq + (a0 - base), a1 - a0, maxg2[j], naccu[j]);
-            }
-          }
+        if (Mu) {
+          const uint32_t a0 = mstu > base ? mstu : base;
+          const uint32_t a1 = mstu + Mu < base + lim ? mstu + Mu : base + lim;
+          if (a0 < a1)
+            ntc_apply(P, Au, gmu, ghatu, W.cij + (a0 - base), W.cur + (a0 - base), W.cp + (a0 - base),
+                      W.cq + (a0 - base), a1 - a0, maxg2, naccu);
         }
         __syncwarp();
       }
-      if (CPL == 1) {
-        if (valid[0] && M[0]) {
-          nacc[0] = naccu[0];
-          const double sgm = P.model == 0 ? P.sigma_c * sqrt((double)maxg2[0]) : P.sigma_c * pow((double)maxg2[0], P.omega1);
-          if (sgm > (double)gm[0]) gm[0] = (float)sgm;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < CPL; j++) { W.mg2[u[j]] = maxg2[j]; W.nacc[u[j]] = naccu[j]; }
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < CPL; j++) {
-          if (valid[j] && M[j]) {
-            const int cl = lane + 32 * j;
-            nacc[j] = W.nacc[cl];
-            const float mg = W.mg2[cl];
-            const double sgm = P.model == 0 ? P.sigma_c * sqrt((double)mg) : P.sigma_c * pow((double)mg, P.omega1);
-            if (sgm > (double)gm[j]) gm[j] = (float)sgm;
-          }
-        }
+      if (valid && M) {
+        nacc = naccu;
+        const double sgm = P.model == 0 ? P.sigma_c * sqrt((double)maxg2) : P.sigma_c * pow((double)maxg2, P.omega1);
+        if (sgm > (double)gm) gm = (float)sgm;
       }
     }
-#pragma unroll
-    for (int j = 0; j < CPL; j++)
-      if (valid[j] && slot >= 0)
-        sample_cell(P, slot, k0 + lane + 32 * j, N[j], SmemCell{wvx + off[j], W.vy + off[j], W.vz + off[j], W.mod + off[j]});
+    if (valid && slot >= 0) sample_cell(P, slot, k, N, SmemCell{wvx + off, W.vy + off, W.vz + off, W.mod + off});
     __syncwarp();
     // ---- F
     if (one_run) {
-      const int hh = h[0];
-      if (reo[0]) {
-        float* __restrict__ dx = (hh ? P0 : P1) + 3 * RS + (int64_t)r[0] * P.stride + (S - rbase[0]);
+      if (reo) {
+        float* __restrict__ dx = (h ? P0 : P1) + 3 * RS + (int64_t)r * P.stride + (S - rbase);
         for (uint32_t q = lane; q < cnt; q += 32) {
           dx[q] = wvx[q];
           dx[RS + q] = W.vy[q];
           dx[2 * RS + q] = W.vz[q];
         }
       } else {
-        float* __restrict__ vxp = (hh ? P1 : P0) + 3 * RS;
+        float* __restrict__ vxp = (h ? P1 : P0) + 3 * RS;
         for (uint32_t q = lane; q < cnt; q += 32) {
           if (W.mod[q]) {
             const uint32_t g = W.sorted[q];
@@ -1286,8 +1183,9 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
       for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
         const uint32_t q = q0 + lane;
         const int cq = q < cnt ? W.cell[q] : 0;
-        const int hq = cell_get<CPL>(h, cq), rq = cell_get<CPL>(reo, cq), runq = cell_get<CPL>(r, cq);
-        const uint32_t bq = cell_get<CPL>(rbase, cq);
+        const int hq = __shfl_sync(FULL, h, cq), rq = __shfl_sync(FULL, reo, cq);
+        const int runq = __shfl_sync(FULL, r, cq);
+        const uint32_t bq = __shfl_sync(FULL, rbase, cq);
         if (q < cnt) {
           if (rq) {
             float* d = (hq ? P0 : P1) + (int64_t)runq * P.stride + (int64_t)(S + q - bq);
@@ -1305,44 +1203,36 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
     }
     if (P.debug)
       for (uint32_t q = lane; q < cnt; q += 32) P.lcr[S + q] = W.sorted[q];
-  } else {
+  } else if (valid) {
     // tile too large for the warp's shared memory: each lane works on its
-    // own cells in global memory (segments sorted in place in LCR)
-#pragma unroll 1
-    for (int j = 0; j < CPL; j++) {
-      if (!valid[j]) continue;
-      uint32_t* seg = P.lcr + st[j];
-      if (N[j] <= 32) insertion_sort(seg, N[j]);
-      else heap_sort(seg, N[j]);
-      GlobCell A{seg, parr(P, h[j], 3), parr(P, h[j], 4), parr(P, h[j], 5)};
-      if (mode == 0) collide_cell(P, run_key(P, r[j]), c[j], (uint32_t)s, N[j], A, gm[j], ncand[j], nacc[j]);
-      if (slot >= 0) sample_cell(P, slot, k0 + lane + 32 * j, N[j], A);
-      if (reo[j]) {
-        for (uint32_t i = 0; i < N[j]; i++) {
-          const uint32_t g = seg[i];
-          const int64_t dst = (int64_t)r[j] * P.stride + (int64_t)(st[j] + i - rbase[j]);
+    // own cell in global memory (segment sorted in place in LCR)
+    uint32_t* seg = P.lcr + st;
+    if (N <= 32) insertion_sort(seg, N);
+    else heap_sort(seg, N);
+    GlobCell A{seg, parr(P, h, 3), parr(P, h, 4), parr(P, h, 5)};
+    if (mode == 0) collide_cell(P, key, c, (uint32_t)s, N, A, gm, ncand, nacc);
+    if (slot >= 0) sample_cell(P, slot, k, N, A);
+    if (reo) {
+      for (uint32_t i = 0; i < N; i++) {
+        const uint32_t g = seg[i];
+        const int64_t dst = (int64_t)r * P.stride + (int64_t)(st + i - rbase);
 #pragma unroll
-          for (int a = 0; a < D; a++) parr(P, h[j] ^ 1, a)[dst] = parr(P, h[j], a)[g];
+        for (int a = 0; a < D; a++) parr(P, h ^ 1, a)[dst] = parr(P, h, a)[g];
 #pragma unroll
-          for (int a = 3; a < 6; a++) parr(P, h[j] ^ 1, a)[dst] = parr(P, h[j], a)[g];
-        }
+        for (int a = 3; a < 6; a++) parr(P, h ^ 1, a)[dst] = parr(P, h, a)[g];
       }
     }
   }
-#pragma unroll
-  for (int j = 0; j < CPL; j++) {
-    const int64_t k = k0 + lane + 32 * j;
-    if (valid[j] && gm[j] != gm0[j]) P.gmax[k] = gm[j];
-    if (valid[j] && P.debug && mode == 0) { P.dbg_cand[k] = ncand[j]; P.dbg_acc[k] = (int32_t)nacc[j]; }
-    // per-run counters: aggregate lanes of the same run
-    if (mode == 0) {
-      const uint32_t rk = valid[j] ? (uint32_t)r[j] : 0xFFFFFFFFu;
-      const unsigned m = __match_any_sync(FULL, rk);
-      const uint32_t sc = __reduce_add_sync(m, ncand[j]), sa = __reduce_add_sync(m, nacc[j]);
-      if (valid[j] && lane == __ffs(m) - 1 && sc) {
-        atomicAdd(&P.ctl.counters[r[j] * 4 + 2], (unsigned long long)sc);
-        atomicAdd(&P.ctl.counters[r[j] * 4 + 3], (unsigned long long)sa);
-      }
+  if (valid && gm != gm0) P.gmax[k] = gm;
+  if (valid && P.debug && mode == 0) { P.dbg_cand[k] = ncand; P.dbg_acc[k] = (int32_t)nacc; }
+  // per-run counters: aggregate lanes of the same run
+  if (mode == 0) {
+    const uint32_t rk = valid ? (uint32_t)r : 0xFFFFFFFFu;
+    const unsigned m = __match_any_sync(FULL, rk);
+    const uint32_t sc = __reduce_add_sync(m, ncand), sa = __reduce_add_sync(m, nacc);
+    if (valid && lane == __ffs(m) - 1 && sc) {
+      atomicAdd(&P.ctl.counters[r * 4 + 2], (unsigned long long)sc);
+      atomicAdd(&P.ctl.counters[r * 4 + 3], (unsigned long long)sa);
     }
   }
 }
@@ -1510,35 +1400,31 @@ void launch_step_mid(const Prm& P, cudaStream_t st) {
   k_step_mid<<<(P.R + 127) / 128, 128, 0, st>>>(P);
 }
 
-template <int D, int NET, int CPL>
+template <int D, int NET>
 static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t st) {
   const int64_t RN = (int64_t)P.R * P.Nc;
-  const int64_t warps = (RN + 32 * CPL - 1) / (32 * CPL);
+  const int64_t warps = (RN + 31) / 32;
   const unsigned g = (unsigned)((warps + WPB - 1) / WPB);
   const size_t smem = WPB * warp_smem_bytes(capw);
   static size_t configured = 0;
   if (smem > configured) {
-    cudaFuncSetAttribute(k_collide<D, NET, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_collide<D, NET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = smem;
   }
-  k_collide<D, NET, CPL><<<g, WPB * 32, smem, st>>>(P, mode, slot, capw);
-}
-
-template <int D>
-static void collide_d(const Prm& P, int mode, int slot, cudaStream_t st) {
-  // register sorting network width: 16 for sparse cells, 32 for dense ones;
-  // cells per lane: 2 (balanced NTC work) unless the tile would not fit
-  if (P.cpl == 2) {
-    if (P.net_wide) collide_t<D, 32, 2>(P, mode, slot, P.capw, st); else collide_t<D, 16, 2>(P, mode, slot, P.capw, st);
-  } else {
-    if (P.net_wide) collide_t<D, 32, 1>(P, mode, slot, P.capw, st); else collide_t<D, 16, 1>(P, mode, slot, P.capw, st);
-  }
+  k_collide<D, NET><<<g, WPB * 32, smem, st>>>(P, mode, slot, capw);
 }
 
 void launch_collide(const Prm& P, int mode, int slot, cudaStream_t st) {
-  if (P.dim == 1) collide_d<1>(P, mode, slot, st);
-  else if (P.dim == 2) collide_d<2>(P, mode, slot, st);
-  else collide_d<3>(P, mode, slot, st);
+  // register sorting network width: 16 for sparse cells, 32 for dense ones
+  const bool wide = P.net_wide != 0;
+  const int capw = P.capw;
+  if (P.dim == 1) {
+    if (wide) collide_t<1, 32>(P, mode, slot, capw, st); else collide_t<1, 16>(P, mode, slot, capw, st);
+  } else if (P.dim == 2) {
+    if (wide) collide_t<2, 32>(P, mode, slot, capw, st); else collide_t<2, 16>(P, mode, slot, capw, st);
+  } else {
+    if (wide) collide_t<3, 32>(P, mode, slot, capw, st); else collide_t<3, 16>(P, mode, slot, capw, st);
+  }
 }
 
 void launch_step_end(const Prm& P, int mode, int slot, cudaStream_t st) {
