@@ -420,22 +420,6 @@ __device__ __forceinline__ bool move_one(const Prm& P, uint2 key, uint32_t idx, 
   return false;
 }
 
-// Runs of equal consecutive keys across the lanes of a warp (the store is
-// near-sorted by cell, so neighbours usually share a key): returns the bit
-// mask of run heads; the head of lane i is 31 - clz(heads & ((2 << i) - 1))
-// and its run ends before the next head.  Cheaper than __match_any_sync.
-__device__ __forceinline__ unsigned run_heads(uint32_t key, int lane) {
-  const uint32_t prev = __shfl_up_sync(FULL, key, 1);
-  return __ballot_sync(FULL, lane == 0 || prev != key);
-}
-__device__ __forceinline__ int run_head_of(unsigned heads, int lane) {
-  return 31 - __clz(heads & (0xFFFFFFFFu >> (31 - lane)));
-}
-__device__ __forceinline__ int run_len_from(unsigned heads, int lane) {  // valid on heads
-  const unsigned above = heads & ~(0xFFFFFFFFu >> (31 - lane));           // heads > lane
-  return (above ? __ffs(above) - 1 : 32) - lane;
-}
-
 // Dynamic work queue for the persistent particle kernels: blocks take items
 // (ITEM consecutive particles of one run, run-major) from a global cursor, so
 // the items in flight stay within a window of ~one run and the cell counters
@@ -535,11 +519,11 @@ __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
       }
       if (i < n) K[i] = kk[j];
     }
-    // warp-aggregated histogram of cell keys (runs of equal neighbours)
+    // warp-aggregated histogram of cell keys
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      const unsigned hd = run_heads(kk[j], lane);
-      if (kk[j] != DEAD_KEY && ((hd >> lane) & 1u)) atomicAdd(&P.cell[kk[j]], (uint32_t)run_len_from(hd, lane));
+      const unsigned m = __match_any_sync(FULL, kk[j]);
+      if (kk[j] != DEAD_KEY && lane == __ffs(m) - 1) atomicAdd(&P.cell[kk[j]], (uint32_t)__popc(m));
     }
   }
 #pragma unroll
@@ -597,6 +581,7 @@ __global__ void k_step_end(Prm P, int mode, int slot) {
 // a chunk are issued before any result is consumed.
 __global__ void __launch_bounds__(256) k_scatter(Prm P) {
   const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
   const int64_t items_per_run = (P.cap + ITEM - 1) / ITEM;
   const int64_t n_items = items_per_run * P.R;
   __shared__ int64_t s_item;
@@ -608,27 +593,25 @@ __global__ void __launch_bounds__(256) k_scatter(Prm P) {
     if (ibase >= n) continue;
     const int64_t base = (int64_t)r * P.stride;
     const uint32_t* K = P.key + base;
-    for (int64_t i0w = ibase + (threadIdx.x >> 5) * 256; i0w < ibase + ITEM && i0w < n; i0w += 2048) {
-      uint32_t kk[8], hd[8], p0[8];
+    for (int64_t i0w = ibase + (threadIdx.x >> 5) * 128; i0w < ibase + ITEM && i0w < n; i0w += 1024) {
+    uint32_t kk[4], m[4], p0[4];
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const int64_t i = i0w + j * 32 + lane;
-        kk[j] = i < n ? K[i] : DEAD_KEY;
-      }
+    for (int j = 0; j < 4; j++) {
+      const int64_t i = i0w + j * 32 + lane;
+      kk[j] = i < n ? K[i] : DEAD_KEY;
+    }
 #pragma unroll
-      for (int j = 0; j < 8; j++) hd[j] = run_heads(kk[j], lane);
+    for (int j = 0; j < 4; j++) m[j] = __match_any_sync(FULL, kk[j]);
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        p0[j] = 0;
-        if (kk[j] != DEAD_KEY && ((hd[j] >> lane) & 1u))
-          p0[j] = atomicAdd(&P.cell[kk[j]], (uint32_t)run_len_from(hd[j], lane));
-      }
+    for (int j = 0; j < 4; j++) {
+      p0[j] = 0;
+      if (kk[j] != DEAD_KEY && lane == __ffs(m[j]) - 1) p0[j] = atomicAdd(&P.cell[kk[j]], (uint32_t)__popc(m[j]));
+    }
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const int head = run_head_of(hd[j], lane);
-        const uint32_t b = __shfl_sync(FULL, p0[j], head);
-        if (kk[j] != DEAD_KEY) P.lcr[b + (uint32_t)(lane - head)] = (uint32_t)(base + i0w + j * 32 + lane);
-      }
+    for (int j = 0; j < 4; j++) {
+      const uint32_t b = __shfl_sync(FULL, p0[j], __ffs(m[j]) - 1);
+      if (kk[j] != DEAD_KEY) P.lcr[b + __popc(m[j] & lt)] = (uint32_t)(base + i0w + j * 32 + lane);
+    }
     }
   }
   queue_done(P.ctl.queue + 2);
