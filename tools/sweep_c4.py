@@ -1,0 +1,30 @@
+"""c4 batching sweep (BASELINE configs[3]): particle-steps/s vs n on one GPU.
+Writes profiles/<tag>_c4_sweep.md.  usage: python tools/sweep_c4.py TAG"""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+rows = []
+for n in (1, 4, 16, 64, 256):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--n-runs", str(n), "--steps", "20",
+                          "--warmup", "3", "--no-cpu", "--no-e2e"], capture_output=True, text=True)
+    line = [l for l in out.stdout.strip().split("\n") if l.startswith("{")]
+    if not line:
+        rows.append((n, None, out.stderr[-300:]))
+        continue
+    d = json.loads(line[-1])
+    rows.append((n, d, None))
+lines = [f"# {tag}: c4 batching sweep (64^3 cells x 10 ppc per run, HS, K=4, 20 timed steps)\n",
+         "| n runs | particles | ms/step | particle-steps/s | collide share | collide GB/s (alg.) |", "|---|---|---|---|---|---|"]
+for n, d, err in rows:
+    if d is None:
+        lines.append(f"| {n} | error | | | | {err} |")
+        continue
+    k = d["roofline"]["kernels"]["k_collide"]
+    lines.append(f"| {n} | {n * 2621440:,} | {d['ms_per_step']:.3f} | {d['value']:.4g} | {k['share']:.2f} | {k['GB/s']} |")
+txt = "\n".join(lines) + "\n"
+print(txt)
+open(os.path.join(ROOT, "profiles", f"{tag}_c4_sweep.md"), "w").write(txt)
