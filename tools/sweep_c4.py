@@ -1,5 +1,5 @@
 """c4 batching sweep (BASELINE configs[3]): particle-steps/s vs n on one GPU.
-Writes profiles/<tag>_c4_sweep.md.  usage: python tools/sweep_c4.py TAG"""
+Writes gpurun_out/<tag>_c4_sweep.md (copied into profiles/).  usage: python tools/sweep_c4.py TAG"""
 import json
 import os
 import subprocess
@@ -27,4 +27,5 @@ for n, d, err in rows:
     lines.append(f"| {n} | {n * 2621440:,} | {d['ms_per_step']:.3f} | {d['value']:.4g} | {k['share']:.2f} | {k['GB/s']} |")
 txt = "\n".join(lines) + "\n"
 print(txt)
-open(os.path.join(ROOT, "profiles", f"{tag}_c4_sweep.md"), "w").write(txt)
+os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+open(os.path.join(ROOT, "gpurun_out", f"{tag}_c4_sweep.md"), "w").write(txt)  # copied into profiles/ afterwards
