@@ -42,9 +42,9 @@ struct Layout {
   int64_t Nc, stride, RN;
   int32_t n_face;
   // ctl offsets
-  size_t c_step, c_status, c_nstore, c_parity, c_reorder, c_inserted, c_counters, c_live, c_psteps, c_slot, c_queue;
+  size_t c_step, c_status, c_nstore, c_parity, c_reorder, c_inserted, c_counters, c_live, c_psteps, c_slot, c_queue, c_heavy;
   // scratch offsets
-  size_t s_face_j, s_face_k, s_open, s_kept, s_part, s_macros, s_cand, s_acc;
+  size_t s_face_j, s_face_k, s_open, s_kept, s_part, s_macros, s_heavy, s_cand, s_acc;
 };
 
 // face-cell lists of the x- face (reading R8)
@@ -148,6 +148,7 @@ int make_layout(const dsmc_problem* p, int debug, Layout& L) {
   L.c_psteps = o; o = align_up(o + 8 * R, 16);
   L.c_slot = o; o = align_up(o + 4 * (size_t)(s.n_slots > 0 ? s.n_slots : 1), 16);
   L.c_queue = o; o = align_up(o + 8 * 8, 16);
+  L.c_heavy = o; o = align_up(o + 4 * 4, 16);
   s.ctl = o;
   const size_t F = (size_t)p->ny * p->nz;
   o = 0;
@@ -158,6 +159,7 @@ int make_layout(const dsmc_problem* p, int debug, Layout& L) {
   const int64_t Lscan = L.RN > L.Nc ? L.RN : L.Nc;
   L.s_part = o; o = align_up(o + 4 * ((size_t)dsmc::scan_tiles(Lscan) + 1), 256);
   L.s_macros = o; o = align_up(o + 8 * 10 * (size_t)L.Nc, 256);
+  L.s_heavy = o; o = align_up(o + 4 * ((size_t)(L.RN + 31) / 32 + 1), 256);
   if (debug) {
     L.s_cand = o; o = align_up(o + 8 * (size_t)L.RN, 256);
     L.s_acc = o; o = align_up(o + 4 * (size_t)L.RN, 256);
@@ -327,6 +329,9 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   P.ctl.psteps = (unsigned long long*)(ct + L.c_psteps);
   P.ctl.slot_done = (int32_t*)(ct + L.c_slot);
   P.ctl.queue = (unsigned long long*)(ct + L.c_queue);
+  P.ctl.heavy = (uint32_t*)(ct + L.c_heavy);
+  P.heavy_list = (uint32_t*)(sc + L.s_heavy);
+  P.caph = 8192;
 
   auto bail = [&](int code) { delete c; return code; };
   std::vector<int32_t> fj, fk;

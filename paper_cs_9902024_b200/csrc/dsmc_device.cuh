@@ -36,6 +36,7 @@ struct Ctl {
   unsigned long long* psteps;    // [R] sum over steps of live particles after Generation
   int32_t* slot_done;        // [n_slots]
   unsigned long long* queue; // [4][2] work-queue cursors (item, blocks done) per persistent kernel
+  uint32_t* heavy;           // [2] heavy-tile queue: count, next
 };
 
 struct Prm {
@@ -90,6 +91,8 @@ struct Prm {
   int32_t debug;
   int32_t net_wide;          // k_collide sorts segments of <= 32 (else 16) in registers
   int32_t capw;              // particles a warp tile (32 cells) stages in shared memory
+  int32_t caph;              // particles k_collide_heavy stages per tile
+  uint32_t* heavy_list;      // [R*Nc/32] tiles k_collide handed to k_collide_heavy
   int64_t* dbg_cand;         // [R*Nc]
   int32_t* dbg_acc;          // [R*Nc]
   Ctl ctl;

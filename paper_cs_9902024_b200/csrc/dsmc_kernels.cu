@@ -552,6 +552,7 @@ __device__ __forceinline__ uint32_t run_lcr_base(const Prm& P, int r) {
 
 __global__ void k_step_end(Prm P, int mode, int slot) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == 0) { P.ctl.heavy[0] = 0; P.ctl.heavy[1] = 0; }   // heavy-tile queue of k_collide
   if (mode == 1) {  // explicit sample
     if (r == 0) P.ctl.slot_done[slot] = 1;
     return;
@@ -1203,6 +1204,11 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
     }
     if (P.debug)
       for (uint32_t q = lane; q < cnt; q += 32) P.lcr[S + q] = W.sorted[q];
+  } else if (P.heavy_list) {
+    // tile too large for the warp's shared memory: hand it to k_collide_heavy
+    // (a whole block with a large staging area -- the "heap" of TLPDPR)
+    if (lane == 0) P.heavy_list[atomicAdd(P.ctl.heavy, 1u)] = (uint32_t)(k0 / 32);
+    return;
   } else if (valid) {
     // tile too large for the warp's shared memory: each lane works on its
     // own cell in global memory (segment sorted in place in LCR)
@@ -1233,6 +1239,242 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
     if (valid && lane == __ffs(m) - 1 && sc) {
       atomicAdd(&P.ctl.counters[r * 4 + 2], (unsigned long long)sc);
       atomicAdd(&P.ctl.counters[r * 4 + 3], (unsigned long long)sa);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_collide_heavy: the warp tiles k_collide could not stage (dense cells, e.g.
+// c5's orifice jet).  The GPU analog of TLPDPR's processor heap (PAPER.md
+// 501-515, Eq. 12): a persistent block "borrows" 256 threads and a large
+// shared-memory staging area for one such tile at a time, taken from the
+// queue k_collide filled.  Same phases and arithmetic as k_collide:
+// block-parallel staging, rank sort, gather and candidate pre-draws; the
+// per-cell candidate walk stays sequential (thread per cell).
+constexpr int HT = 256;     // threads per heavy block
+constexpr int CCH = 1024;   // pre-drawn candidates per round
+
+__host__ __device__ inline size_t heavy_smem_bytes(int caph) { return (size_t)caph * 18 + (size_t)CCH * 16 + 16; }
+
+template <int D>
+__global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_arg, int caph) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  uint32_t* s_sorted = reinterpret_cast<uint32_t*>(dsm);
+  uint32_t* s_a = s_sorted + caph;
+  float* s_vx = reinterpret_cast<float*>(s_a);
+  float* s_vy = reinterpret_cast<float*>(s_a + caph);
+  float* s_vz = s_vy + caph;
+  uint32_t* s_cij = reinterpret_cast<uint32_t*>(s_vz + caph);
+  uint32_t* s_cur = s_cij + CCH;
+  float* s_cp = reinterpret_cast<float*>(s_cur + CCH);
+  float* s_cq = s_cp + CCH;
+  uint8_t* s_cell = reinterpret_cast<uint8_t*>(s_cq + CCH);
+  uint8_t* s_mod = s_cell + caph;
+  __shared__ uint32_t c_st[33], c_N[32], c_M[32], c_mst[33], c_c[32], c_base[32];
+  __shared__ int c_r[32], c_h[32], c_reo[32];
+  __shared__ float c_gm[32];
+  __shared__ uint32_t s_tile, s_warp[HT / 32];
+  const int t = threadIdx.x;
+  const int64_t RN = (int64_t)P.R * P.Nc;
+  const int64_t RS = (int64_t)P.R * P.stride;
+  const uint32_t Nc32 = (uint32_t)P.Nc;
+  const int32_t s = *P.ctl.step;
+  int slot = -1;
+  if (mode == 0) {
+    if ((s + 1) % P.sample_every == 0 && (s + 1) / P.sample_every - 1 < P.n_slots) slot = (s + 1) / P.sample_every - 1;
+  } else {
+    slot = slot_arg;
+  }
+  const uint32_t n_heavy = *P.ctl.heavy;
+  for (;;) {
+    __syncthreads();
+    if (t == 0) s_tile = atomicAdd(P.ctl.heavy + 1, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= n_heavy) break;
+    const int64_t k0 = (int64_t)P.heavy_list[tile] * 32;
+    // ---- A (thread per cell)
+    const bool valid = t < 32 && k0 + t < RN;
+    uint32_t N = 0, c = 0;
+    int r = 0, h = 0, reo = 0;
+    float gm = 0.0f;
+    if (t < 32) {
+      const int64_t k = k0 + t;
+      uint32_t st = 0, en = 0;
+      if (valid) {
+        st = k == 0 ? 0u : P.cell[k - 1];
+        en = P.cell[k];
+        r = (int)((uint32_t)k / Nc32);
+        c = (uint32_t)k - (uint32_t)r * Nc32;
+        h = P.ctl.parity[r];
+        reo = mode == 0 ? P.ctl.reorder[r] : 0;
+        gm = P.gmax[k];
+        c_base[t] = run_lcr_base(P, r);
+      } else {
+        st = en = 0xFFFFFFFFu;
+      }
+      N = en - st;
+      c_st[t] = st;
+      c_N[t] = valid ? N : 0u;
+      c_c[t] = c;
+      c_r[t] = r;
+      c_h[t] = h;
+      c_reo[t] = reo;
+      c_gm[t] = gm;
+    }
+    __syncthreads();
+    int last = 31;
+    while (c_st[last] == 0xFFFFFFFFu) last--;
+    const uint32_t S = c_st[0], E = c_st[last] + c_N[last], cnt = E - S;
+    if (t == 32) c_st[32] = E;
+    __syncthreads();
+    const float gm0 = gm;
+    uint32_t ncand = 0, nacc = 0;
+    if (cnt <= (uint32_t)caph) {
+      // ---- B: stage the LCR slice, tag each element with its cell
+      for (uint32_t q = t; q < cnt; q += HT) {
+        s_a[q] = P.lcr[S + q];
+        int lo = 0;
+#pragma unroll
+        for (int stp = 16; stp > 0; stp >>= 1)
+          if (lo + stp <= last && c_st[lo + stp] <= S + q) lo += stp;
+        s_cell[q] = (uint8_t)lo;
+      }
+      __syncthreads();
+      // ---- C: rank of every element inside its segment
+      for (uint32_t q = t; q < cnt; q += HT) {
+        const int cq = s_cell[q];
+        const uint32_t b = c_st[cq] - S, n = c_N[cq], v = s_a[q];
+        uint32_t rank = 0;
+        for (uint32_t p = 0; p < n; p++) rank += s_a[b + p] < v ? 1u : 0u;
+        s_sorted[b + rank] = v;
+      }
+      __syncthreads();
+      // ---- D: gather velocities (and move positions on reorder steps)
+      for (uint32_t q = t; q < cnt; q += HT) {
+        const int cq = s_cell[q];
+        const int hq = c_h[cq];
+        const uint32_t g = s_sorted[q];
+        const float* src = P.P + (int64_t)hq * P.half + g;
+        if (c_reo[cq]) {
+          float* d = P.P + (int64_t)(hq ^ 1) * P.half + (int64_t)c_r[cq] * P.stride + (int64_t)(S + q - c_base[cq]);
+#pragma unroll
+          for (int a = 0; a < D; a++) d[a * RS] = src[a * RS];
+        }
+        const float vx = src[3 * RS], vy = src[4 * RS], vz = src[5 * RS];
+        s_vx[q] = vx;
+        s_vy[q] = vy;
+        s_vz[q] = vz;
+        s_mod[q] = 0;
+      }
+      __syncthreads();
+      // ---- E: NTC
+      if (mode == 0) {
+        uint32_t M = 0;
+        if (valid) M = ntc_count(P, run_key(P, r), c, (uint32_t)s, N, gm);
+        ncand = M;
+        if (t < 32) {
+          uint32_t x = M;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, x, o); if (t >= o) x += y; }
+          c_mst[t] = x - M;
+          c_M[t] = M;
+          if (t == 31) c_mst[32] = x;
+        }
+        __syncthreads();
+        const uint32_t tot = c_mst[32];
+        const uint32_t off = t < 32 ? c_st[t] - S : 0u;
+        const double gmd = (double)gm, ghat = gmd / P.sigma_c;
+        float maxg2 = 0.0f;
+        uint32_t naccu = 0;
+        for (uint32_t base = 0; base < tot; base += CCH) {
+          const uint32_t lim = tot - base < (uint32_t)CCH ? tot - base : (uint32_t)CCH;
+          for (uint32_t q = t; q < lim; q += HT) {
+            const uint32_t gq = base + q;
+            int lo = 0;
+#pragma unroll
+            for (int stp = 16; stp > 0; stp >>= 1)
+              if (lo + stp < 32 && c_mst[lo + stp] <= gq) lo += stp;
+            const uint32_t nc = c_N[lo], kq = gq - c_mst[lo];
+            const uint2 keyc = run_key(P, c_r[lo]);
+            const uint4 w = draw(keyc, c_c[lo], (uint32_t)s, TAG_COLL_PAIR, kq, 0);
+            const uint32_t i = lemire(w.x, nc);
+            uint32_t j = lemire(w.y, nc - 1);
+            if (j >= i) j++;
+            s_cij[q] = i | (j << 16);
+            s_cur[q] = w.z;
+            marsaglia_pq(keyc, c_c[lo], (uint32_t)s, kq, s_cp[q], s_cq[q]);
+          }
+          __syncthreads();
+          if (valid && M) {
+            const uint32_t mst = c_mst[t];
+            const uint32_t a0 = mst > base ? mst : base;
+            const uint32_t a1 = mst + M < base + lim ? mst + M : base + lim;
+            if (a0 < a1) {
+              SmemCell A{s_vx + off, s_vy + off, s_vz + off, s_mod + off};
+              ntc_apply(P, A, gmd, ghat, s_cij + (a0 - base), s_cur + (a0 - base), s_cp + (a0 - base),
+                        s_cq + (a0 - base), a1 - a0, maxg2, naccu);
+            }
+          }
+          __syncthreads();
+        }
+        if (valid && M) {
+          nacc = naccu;
+          const double sgm = P.model == 0 ? P.sigma_c * sqrt((double)maxg2) : P.sigma_c * pow((double)maxg2, P.omega1);
+          if (sgm > gmd) gm = (float)sgm;
+        }
+      }
+      if (valid && slot >= 0) {
+        const uint32_t off = c_st[t] - S;
+        sample_cell(P, slot, k0 + t, N, SmemCell{s_vx + off, s_vy + off, s_vz + off, s_mod + off});
+      }
+      __syncthreads();
+      // ---- F: write back
+      for (uint32_t q = t; q < cnt; q += HT) {
+        const int cq = s_cell[q];
+        const int hq = c_h[cq];
+        if (c_reo[cq]) {
+          float* d = P.P + (int64_t)(hq ^ 1) * P.half + (int64_t)c_r[cq] * P.stride + (int64_t)(S + q - c_base[cq]);
+          d[3 * RS] = s_vx[q];
+          d[4 * RS] = s_vy[q];
+          d[5 * RS] = s_vz[q];
+        } else if (s_mod[q]) {
+          float* d = P.P + (int64_t)hq * P.half + s_sorted[q];
+          d[3 * RS] = s_vx[q];
+          d[4 * RS] = s_vy[q];
+          d[5 * RS] = s_vz[q];
+        }
+        if (P.debug) P.lcr[S + q] = s_sorted[q];
+      }
+    } else if (valid) {
+      // beyond even the heavy staging area: thread per cell in global memory
+      const uint32_t st = c_st[t];
+      uint32_t* seg = P.lcr + st;
+      if (N <= 32) insertion_sort(seg, N);
+      else heap_sort(seg, N);
+      GlobCell A{seg, parr(P, h, 3), parr(P, h, 4), parr(P, h, 5)};
+      if (mode == 0) collide_cell(P, run_key(P, r), c, (uint32_t)s, N, A, gm, ncand, nacc);
+      if (slot >= 0) sample_cell(P, slot, k0 + t, N, A);
+      if (reo) {
+        const uint32_t rb = c_base[t];
+        for (uint32_t i = 0; i < N; i++) {
+          const uint32_t g = seg[i];
+          const int64_t dst = (int64_t)r * P.stride + (int64_t)(st + i - rb);
+#pragma unroll
+          for (int a = 0; a < D; a++) parr(P, h ^ 1, a)[dst] = parr(P, h, a)[g];
+#pragma unroll
+          for (int a = 3; a < 6; a++) parr(P, h ^ 1, a)[dst] = parr(P, h, a)[g];
+        }
+      }
+    }
+    if (valid) {
+      const int64_t k = k0 + t;
+      if (gm != gm0) P.gmax[k] = gm;
+      if (P.debug && mode == 0) { P.dbg_cand[k] = ncand; P.dbg_acc[k] = (int32_t)nacc; }
+      if (mode == 0 && ncand) {
+        atomicAdd(&P.ctl.counters[r * 4 + 2], (unsigned long long)ncand);
+        atomicAdd(&P.ctl.counters[r * 4 + 3], (unsigned long long)nacc);
+      }
     }
   }
 }
@@ -1427,6 +1669,24 @@ void launch_collide(const Prm& P, int mode, int slot, cudaStream_t st) {
   }
 }
 
+template <int D>
+static void heavy_t(const Prm& P, int mode, int slot, cudaStream_t st) {
+  const size_t smem = heavy_smem_bytes(P.caph);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(k_collide_heavy<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  k_collide_heavy<D><<<num_sms(), HT, smem, st>>>(P, mode, slot, P.caph);
+}
+
+void launch_collide_heavy(const Prm& P, int mode, int slot, cudaStream_t st) {
+  if (!P.heavy_list) return;
+  if (P.dim == 1) heavy_t<1>(P, mode, slot, st);
+  else if (P.dim == 2) heavy_t<2>(P, mode, slot, st);
+  else heavy_t<3>(P, mode, slot, st);
+}
+
 void launch_step_end(const Prm& P, int mode, int slot, cudaStream_t st) {
   k_step_end<<<(P.R + 127) / 128, 128, 0, st>>>(P, mode, slot);
 }
@@ -1459,6 +1719,9 @@ void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
   hook.before(KSLOT_COLLIDE);
   launch_collide(P, 0, -1, st);
   hook.after(KSLOT_COLLIDE);
+  hook.before(KSLOT_COLLIDE_HEAVY);
+  launch_collide_heavy(P, 0, -1, st);
+  hook.after(KSLOT_COLLIDE_HEAVY);
   hook.before(KSLOT_STEP_END);
   launch_step_end(P, 0, 0, st);
   hook.after(KSLOT_STEP_END);
@@ -1470,6 +1733,7 @@ void issue_sample(const Prm& P, int slot, cudaStream_t st) {
   launch_scan(P.cell, (int64_t)P.R * P.Nc, P.scan_part, st, LaunchHook{});
   launch_scatter(P, st);
   launch_collide(P, 1, slot, st);
+  launch_collide_heavy(P, 1, slot, st);
   launch_step_end(P, 1, slot, st);
 }
 
@@ -1485,6 +1749,7 @@ const char* kernel_slot_name(int k) {
     case KSLOT_SCAN_DOWN: return "k_scan_down";
     case KSLOT_SCATTER: return "k_scatter";
     case KSLOT_COLLIDE: return "k_collide";
+    case KSLOT_COLLIDE_HEAVY: return "k_collide_heavy";
     case KSLOT_STEP_END: return "k_step_end";
     default: return "";
   }

@@ -19,6 +19,7 @@ enum KernelSlot {
   KSLOT_SCATTER,
   KSLOT_COLLIDE,
   KSLOT_STEP_END,
+  KSLOT_COLLIDE_HEAVY,
   KSLOT_COUNT
 };
 

@@ -129,6 +129,17 @@ def test_one_step_parity_heavy_cells(dsmc_gpu, oracle_mod):
     one_step_case(dsmc_gpu, oracle_mod, p, 0, 2, seed_state=st)
 
 
+def test_one_step_parity_giant_cell(dsmc_gpu, oracle_mod):
+    """A cell beyond even the heavy staging area (9000 > 8192 particles):
+    the per-thread global-memory fallback of k_collide_heavy."""
+    p = configs.get("c4_small")
+    p["reorder_every"] = 1
+    p["fill"] = []
+    st = inputs.clustered_state(6, p, [77], 9000)
+    p["cap_per_run"] = len(st["x"]) + 64
+    one_step_case(dsmc_gpu, oracle_mod, p, 0, 4, seed_state=st)
+
+
 def test_run_independent_of_batch(dsmc_gpu):
     """S:288 'strategies change time, never answers': run r computed alone
     (n=1, run_id0=r) equals run r inside a batch, bit for bit."""
