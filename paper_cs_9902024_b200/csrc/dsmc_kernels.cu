@@ -1254,7 +1254,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
 constexpr int HT = 256;     // threads per heavy block
 constexpr int CCH = 1024;   // pre-drawn candidates per round
 
-__host__ __device__ inline size_t heavy_smem_bytes(int caph) { return (size_t)caph * 18 + (size_t)CCH * 16 + 16; }
+__host__ __device__ inline size_t heavy_smem_bytes(int caph) { return (size_t)caph * 20 + (size_t)CCH * 18 + 16; }
 
 template <int D>
 __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_arg, int caph) {
@@ -1268,9 +1268,13 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
   uint32_t* s_cur = s_cij + CCH;
   float* s_cp = reinterpret_cast<float*>(s_cur + CCH);
   float* s_cq = s_cp + CCH;
-  uint8_t* s_cell = reinterpret_cast<uint8_t*>(s_cq + CCH);
+  uint16_t* s_lw = reinterpret_cast<uint16_t*>(s_cq + CCH);   // last wave that touched a particle
+  uint16_t* s_cw = s_lw + caph;                                  // wave of a candidate
+  uint8_t* s_cell = reinterpret_cast<uint8_t*>(s_cw + CCH);
   uint8_t* s_mod = s_cell + caph;
-  __shared__ uint32_t c_st[33], c_N[32], c_M[32], c_mst[33], c_c[32], c_base[32];
+  __shared__ uint32_t c_st[33], c_N[32], c_M[32], c_mst[33], c_c[32], c_base[32], c_nacc[32];
+  __shared__ float c_mg2[32];
+  __shared__ uint32_t s_wmax;
   __shared__ int c_r[32], c_h[32], c_reo[32];
   __shared__ float c_gm[32];
   __shared__ uint32_t s_tile, s_warp[HT / 32];
@@ -1366,6 +1370,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
         s_vy[q] = vy;
         s_vz[q] = vz;
         s_mod[q] = 0;
+        s_lw[q] = 0;
       }
       __syncthreads();
       // ---- E: NTC
@@ -1384,11 +1389,12 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
         __syncthreads();
         const uint32_t tot = c_mst[32];
         const uint32_t off = t < 32 ? c_st[t] - S : 0u;
-        const double gmd = (double)gm, ghat = gmd / P.sigma_c;
-        float maxg2 = 0.0f;
-        uint32_t naccu = 0;
+        const double gmd = (double)gm;
+        if (t < 32) { c_mg2[t] = 0.0f; c_nacc[t] = 0; }
+        uint32_t wbase = 0;   // waves are numbered across rounds, so s_lw needs no reset
         for (uint32_t base = 0; base < tot; base += CCH) {
           const uint32_t lim = tot - base < (uint32_t)CCH ? tot - base : (uint32_t)CCH;
+          if (t == 0) s_wmax = wbase;
           for (uint32_t q = t; q < lim; q += HT) {
             const uint32_t gq = base + q;
             int lo = 0;
@@ -1406,20 +1412,56 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
             marsaglia_pq(keyc, c_c[lo], (uint32_t)s, kq, s_cp[q], s_cq[q]);
           }
           __syncthreads();
+          // dependency waves (thread per cell, in increasing k): a candidate
+          // runs after every earlier candidate of its cell that shares a particle
           if (valid && M) {
             const uint32_t mst = c_mst[t];
             const uint32_t a0 = mst > base ? mst : base;
             const uint32_t a1 = mst + M < base + lim ? mst + M : base + lim;
-            if (a0 < a1) {
-              SmemCell A{s_vx + off, s_vy + off, s_vz + off, s_mod + off};
-              ntc_apply(P, A, gmd, ghat, s_cij + (a0 - base), s_cur + (a0 - base), s_cp + (a0 - base),
-                        s_cq + (a0 - base), a1 - a0, maxg2, naccu);
+            uint32_t wm = wbase;
+            for (uint32_t q = a0; q < a1; q++) {
+              const uint32_t pr = s_cij[q - base];
+              const uint32_t i = off + (pr & 0xFFFFu), j = off + (pr >> 16);
+              uint32_t w = s_lw[i] > s_lw[j] ? s_lw[i] : s_lw[j];
+              w = (w > wbase ? w : wbase) + 1;
+              s_lw[i] = (uint16_t)w;
+              s_lw[j] = (uint16_t)w;
+              s_cw[q - base] = (uint16_t)w;
+              wm = w > wm ? w : wm;
             }
+            atomicMax(&s_wmax, wm);
           }
           __syncthreads();
+          const uint32_t wend = s_wmax;
+          for (uint32_t wv = wbase + 1; wv <= wend; wv++) {
+            for (uint32_t q = t; q < lim; q += HT) {
+              if (s_cw[q] != wv) continue;
+              const uint32_t gq = base + q;
+              int lo = 0;
+#pragma unroll
+              for (int stp = 16; stp > 0; stp >>= 1)
+                if (lo + stp < 32 && c_mst[lo + stp] <= gq) lo += stp;
+              const uint32_t o = c_st[lo] - S;
+              const double gml = (double)c_gm[lo];
+              SmemCell A{s_vx + o, s_vy + o, s_vz + o, s_mod + o};
+              float mg = 0.0f;
+              uint32_t na = 0;
+              ntc_apply(P, A, gml, gml / P.sigma_c, s_cij + q, s_cur + q, s_cp + q, s_cq + q, 1, mg, na);
+              atomicMax(reinterpret_cast<uint32_t*>(&c_mg2[lo]), __float_as_uint(mg));  // g^2 >= 0: int order
+              if (na) atomicAdd(&c_nacc[lo], na);
+            }
+            __syncthreads();
+          }
+          wbase = wend;
+          if (wbase > 60000u) {  // keep the 16-bit wave ids in range: reset between rounds
+            for (uint32_t q = t; q < cnt; q += HT) s_lw[q] = 0;
+            wbase = 0;
+            __syncthreads();
+          }
         }
         if (valid && M) {
-          nacc = naccu;
+          nacc = c_nacc[t];
+          const float maxg2 = c_mg2[t];
           const double sgm = P.model == 0 ? P.sigma_c * sqrt((double)maxg2) : P.sigma_c * pow((double)maxg2, P.omega1);
           if (sgm > gmd) gm = (float)sgm;
         }
