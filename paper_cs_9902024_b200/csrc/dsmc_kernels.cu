@@ -946,6 +946,12 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
   }
   const uint2 key = run_key(P, r);
   uint32_t ncand = 0, nacc = 0;
+  if (cnt > (uint32_t)capw && P.heavy_list) {
+    // tile too large for the warp's shared memory: hand it to k_collide_heavy
+    // (a whole block with a large staging area -- the "heap" of TLPDPR)
+    if (lane == 0) P.heavy_list[atomicAdd(P.ctl.heavy, 1u)] = (uint32_t)(k0 / 32);
+    return;
+  }
   float gm = valid ? P.gmax[k] : 0.0f;
   const float gm0 = gm;
   if (cnt <= (uint32_t)capw) {
@@ -1204,11 +1210,6 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
     }
     if (P.debug)
       for (uint32_t q = lane; q < cnt; q += 32) P.lcr[S + q] = W.sorted[q];
-  } else if (P.heavy_list) {
-    // tile too large for the warp's shared memory: hand it to k_collide_heavy
-    // (a whole block with a large staging area -- the "heap" of TLPDPR)
-    if (lane == 0) P.heavy_list[atomicAdd(P.ctl.heavy, 1u)] = (uint32_t)(k0 / 32);
-    return;
   } else if (valid) {
     // tile too large for the warp's shared memory: each lane works on its
     // own cell in global memory (segment sorted in place in LCR)

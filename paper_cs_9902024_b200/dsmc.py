@@ -114,9 +114,10 @@ SIGNATURES = [
 ]
 
 
-def load_library(path=LIB_PATH):
-    """Load libdsmc.so; raises (never falls back) if it is missing."""
+def load_library(path=None):
+    """Load libdsmc.so (or $DSMC_LIB, for A/B builds); raises, never falls back."""
     global _lib
+    path = path or os.environ.get("DSMC_LIB") or LIB_PATH
     if _lib is None:
         if not os.path.exists(path):
             raise DsmcError(-7, f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
