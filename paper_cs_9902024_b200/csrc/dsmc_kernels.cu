@@ -1120,10 +1120,8 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
             cc[hh] = __shfl_sync(FULL, c, lo);
           }
           uint4 wp[2], wd[2];
-          const bool second = q0 + 32 < lim;   // warp-uniform: skip an empty half pass
 #pragma unroll
           for (int hh = 0; hh < 2; hh++) {
-            if (hh == 1 && !second) { wp[1] = wp[0]; wd[1] = wd[0]; continue; }
             const uint2 keyc = run_key(P, rc[hh]);
             wp[hh] = draw(keyc, cc[hh], (uint32_t)s, TAG_COLL_PAIR, kq[hh], 0);
             wd[hh] = draw(keyc, cc[hh], (uint32_t)s, TAG_COLL_DIR, kq[hh], 0);

@@ -42,8 +42,8 @@ def find(m):
 kstart = find("k_collide(Prm P, int mode, int slot_arg, int capw) {")
 marks = [("A", kstart), ("B", find("    // ---- B")), ("C", find("    // ---- C")), ("D", find("    // ---- D")),
          ("E0", find("    // ---- E")), ("E1", find("      for (uint32_t base = 0; base < tot; base += CCW) {")),
-         ("E2", find("        if (Mu) {")), ("Efin", find("      if (valid && M) {\n        nacc = naccu;") if False else find("        nacc = naccu;")),
-         ("F", find("    // ---- F")), ("G", find("own cell in global memory (segment sorted in place in LCR)")),
+         ("E2", find("        if (Mu) {")), ("Efin", find("      W.mg2[u] = maxg2;")),
+         ("F", find("    // ---- F")), ("G", find("tile too large for the warp")),
          ("end", find("// per-run counters: aggregate") + 12)]
 fns = [("marsaglia_pq", find("__device__ __forceinline__ void marsaglia_pq")),
        ("ntc_apply", find("// candidates k in [k_lo, k_hi)")), ("sort_net", find("template <int NN>")),
