@@ -20,6 +20,7 @@ enum KernelSlot {
   KSLOT_COLLIDE,
   KSLOT_STEP_END,
   KSLOT_COLLIDE_HEAVY,
+  KSLOT_STAGE,
   KSLOT_COUNT
 };
 
