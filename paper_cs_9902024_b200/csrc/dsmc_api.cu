@@ -44,7 +44,7 @@ struct Layout {
   // ctl offsets
   size_t c_step, c_status, c_nstore, c_parity, c_reorder, c_inserted, c_counters, c_live, c_psteps, c_slot, c_queue, c_heavy;
   // scratch offsets
-  size_t s_face_j, s_face_k, s_open, s_kept, s_part, s_macros, s_heavy, s_stage, s_cand, s_acc;
+  size_t s_face_j, s_face_k, s_open, s_kept, s_part, s_macros, s_heavy, s_cand, s_acc;
 };
 
 // face-cell lists of the x- face (reading R8)
@@ -160,7 +160,6 @@ int make_layout(const dsmc_problem* p, int debug, Layout& L) {
   L.s_part = o; o = align_up(o + 4 * ((size_t)dsmc::scan_tiles(Lscan) + 1), 256);
   L.s_macros = o; o = align_up(o + 8 * 10 * (size_t)L.Nc, 256);
   L.s_heavy = o; o = align_up(o + 4 * ((size_t)(L.RN + 31) / 32 + 1), 256);
-  L.s_stage = o; o = align_up(o + 3 * 4 * (size_t)p->n_runs * (size_t)L.stride, 256);
   if (debug) {
     L.s_cand = o; o = align_up(o + 8 * (size_t)L.RN, 256);
     L.s_acc = o; o = align_up(o + 4 * (size_t)L.RN, 256);
@@ -332,10 +331,6 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   P.ctl.queue = (unsigned long long*)(ct + L.c_queue);
   P.ctl.heavy = (uint32_t*)(ct + L.c_heavy);
   P.heavy_list = (uint32_t*)(sc + L.s_heavy);
-  {
-    const char* e = std::getenv("DSMC_SPLIT");
-    P.stage = (e && e[0] == '0') ? nullptr : (float*)(sc + L.s_stage);
-  }
   P.caph = 8192;
 
   auto bail = [&](int code) { delete c; return code; };

@@ -93,7 +93,6 @@ struct Prm {
   int32_t capw;              // particles a warp tile (32 cells) stages in shared memory
   int32_t caph;              // particles k_collide_heavy stages per tile
   uint32_t* heavy_list;      // [R*Nc/32] tiles k_collide handed to k_collide_heavy
-  float* stage;              // [3][R*stride] velocities in LCR order (split Interaction), or null
   int64_t* dbg_cand;         // [R*Nc]
   int32_t* dbg_acc;          // [R*Nc]
   Ctl ctl;

@@ -1245,357 +1245,6 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
 }
 
 // ---------------------------------------------------------------------------
-// Split Interaction (mode 0 steps): C1 = k_stage, C2 = k_ntc.
-// k_stage is the latency-bound half -- canonical sort and velocity gather --
-// with few registers and a small shared footprint, so many warps hide the
-// dependent loads; it writes each tile's velocities contiguously in LCR order
-// (into the staging buffer, or on reorder steps straight into the other half
-// of P at the canonical rank, positions too).  k_ntc is the compute half: one
-// batch of coalesced loads of that contiguous slice, then NTC, Sampling and
-// the write-back of the pairs that collided.  Both use the same warp tiles
-// and capacity as k_collide; tiles beyond it go to k_collide_heavy.
-constexpr int SWPB = 8;     // warps per block in k_stage
-
-__host__ __device__ inline size_t stage_smem_bytes(int capw) { return (size_t)capw * 9 + 16; }
-
-template <int D, int NET>
-__global__ void __launch_bounds__(SWPB * 32, 3) k_stage(Prm P, int capw) {
-  extern __shared__ __align__(16) uint8_t dsm[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t* s_a = reinterpret_cast<uint32_t*>(dsm + (size_t)wid * stage_smem_bytes(capw));
-  uint32_t* s_sorted = s_a + capw;
-  uint8_t* s_cell = reinterpret_cast<uint8_t*>(s_sorted + capw);
-  const int64_t RN = (int64_t)P.R * P.Nc;
-  const int64_t RS = (int64_t)P.R * P.stride;
-  float* const P0 = P.P;
-  float* const P1 = P.P + P.half;
-  const int64_t k0 = ((int64_t)blockIdx.x * SWPB + wid) * 32;
-  if (k0 >= RN) return;
-  const int64_t k = k0 + lane;
-  const bool valid = k < RN;
-  const int64_t klast = k0 + 31 < RN ? k0 + 31 : RN - 1;
-  const int last_lane = (int)(klast - k0);
-  const uint32_t Nc32 = (uint32_t)P.Nc;
-  const int r_first = (int)((uint32_t)k0 / Nc32);
-  const bool one_run = r_first == (int)((uint32_t)klast / Nc32);
-  uint32_t st = 0, en = 0;
-  if (valid) {
-    st = k == 0 ? 0u : P.cell[k - 1];
-    en = P.cell[k];
-  }
-  const int r = valid ? (int)((uint32_t)k / Nc32) : (int)((uint32_t)klast / Nc32);
-  const uint32_t N = en - st;
-  const uint32_t S = __shfl_sync(FULL, st, 0);
-  const uint32_t E = __shfl_sync(FULL, en, last_lane);
-  const uint32_t cnt = E - S;
-  if (cnt > (uint32_t)capw) {
-    if (lane == 0) P.heavy_list[atomicAdd(P.ctl.heavy, 1u)] = (uint32_t)(k0 / 32);
-    return;
-  }
-  const uint32_t off = st - S;
-  const int h = P.ctl.parity[r];
-  const int reo = P.ctl.reorder[r];
-  const uint32_t rbase = run_lcr_base(P, r);
-  // ---- B
-  for (uint32_t q0 = 0; q0 < cnt; q0 += 256) {
-    uint32_t v[8];
-#pragma unroll
-    for (int u = 0; u < 8; u++) {
-      const uint32_t q = q0 + 32 * u + lane;
-      if (q < cnt) v[u] = P.lcr[S + q];
-    }
-#pragma unroll
-    for (int u = 0; u < 8; u++) {
-      const uint32_t q = q0 + 32 * u + lane;
-      if (q < cnt) s_a[q] = v[u];
-    }
-  }
-  if (valid) for (uint32_t i = 0; i < N; i++) s_cell[off + i] = (uint8_t)lane;
-  __syncwarp();
-  // ---- C
-  if (valid && N <= (uint32_t)NET) {
-    uint32_t v[NET];
-#pragma unroll
-    for (int i = 0; i < NET; i++) v[i] = (uint32_t)i < N ? s_a[off + i] : 0xFFFFFFFFu;
-    sort_net<NET>(v);
-#pragma unroll
-    for (int i = 0; i < NET; i++) if ((uint32_t)i < N) s_sorted[off + i] = v[i];
-  }
-  if (__any_sync(FULL, valid && N > (uint32_t)NET)) {
-    for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
-      const uint32_t q = q0 + lane;
-      const int cq = q < cnt ? s_cell[q] : 0;
-      const uint32_t n = __shfl_sync(FULL, N, cq), b = __shfl_sync(FULL, off, cq);
-      if (q < cnt && n > (uint32_t)NET) {
-        const uint32_t v = s_a[q];
-        uint32_t rank = 0;
-        for (uint32_t p = 0; p < n; p++) rank += s_a[b + p] < v ? 1u : 0u;
-        s_sorted[b + rank] = v;
-      }
-    }
-  }
-  __syncwarp();
-  // ---- D: gather in canonical order, written contiguously (LCR position p = S + q)
-  if (one_run) {
-    const float* __restrict__ src = (h ? P1 : P0);
-    float* __restrict__ vdst = reo ? (h ? P0 : P1) + 3 * RS + (int64_t)r * P.stride - rbase : P.stage;
-    float* __restrict__ xdst = (h ? P0 : P1) + (int64_t)r * P.stride - rbase;
-    const bool write_lcr = !reo || P.debug;
-    for (uint32_t q0 = 0; q0 < cnt; q0 += 256) {
-      uint32_t gg[8];
-      float vv[8][3];
-#pragma unroll
-      for (int u = 0; u < 8; u++) {
-        const uint32_t q = q0 + 32 * u + lane;
-        gg[u] = q < cnt ? s_sorted[q] : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; u++) {
-        if (q0 + 32 * u + lane < cnt) {
-#pragma unroll
-          for (int a = 0; a < 3; a++) vv[u][a] = src[(3 + a) * RS + gg[u]];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; u++) {
-        const uint32_t q = q0 + 32 * u + lane;
-        if (q < cnt) {
-          const int64_t p = (int64_t)S + q;
-#pragma unroll
-          for (int a = 0; a < 3; a++) vdst[a * RS + p] = vv[u][a];
-          if (write_lcr) P.lcr[p] = gg[u];
-        }
-      }
-      if (reo) {
-#pragma unroll
-        for (int a = 0; a < D; a++) {
-          float xs[8];
-#pragma unroll
-          for (int u = 0; u < 8; u++)
-            if (q0 + 32 * u + lane < cnt) xs[u] = src[a * RS + gg[u]];
-#pragma unroll
-          for (int u = 0; u < 8; u++) {
-            const uint32_t q = q0 + 32 * u + lane;
-            if (q < cnt) xdst[a * RS + S + q] = xs[u];
-          }
-        }
-      }
-    }
-  } else {
-    for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
-      const uint32_t q = q0 + lane;
-      const int cq = q < cnt ? s_cell[q] : 0;
-      const int hq = __shfl_sync(FULL, h, cq), rq = __shfl_sync(FULL, reo, cq), runq = __shfl_sync(FULL, r, cq);
-      const uint32_t bq = __shfl_sync(FULL, rbase, cq);
-      if (q < cnt) {
-        const uint32_t g = s_sorted[q];
-        const float* src = (hq ? P1 : P0) + g;
-        const int64_t p = (int64_t)S + q;
-        float* vdst = rq ? (hq ? P0 : P1) + 3 * RS + (int64_t)runq * P.stride - bq : P.stage;
-        vdst[p] = src[3 * RS];
-        vdst[RS + p] = src[4 * RS];
-        vdst[2 * RS + p] = src[5 * RS];
-        if (!rq || P.debug) P.lcr[p] = g;
-        if (rq) {
-          float* d = (hq ? P0 : P1) + (int64_t)runq * P.stride - bq + p;
-#pragma unroll
-          for (int a = 0; a < D; a++) d[a * RS] = src[a * RS];
-        }
-      }
-    }
-  }
-}
-
-template <int D>
-__global__ void __launch_bounds__(WPB * 32) k_ntc(Prm P, int capw) {
-  extern __shared__ __align__(16) uint8_t dsm[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const WarpSmem W = warp_smem(dsm + (size_t)wid * warp_smem_bytes(capw), capw);
-  const int64_t RN = (int64_t)P.R * P.Nc;
-  const int64_t RS = (int64_t)P.R * P.stride;
-  float* const P0 = P.P;
-  float* const P1 = P.P + P.half;
-  const int64_t k0 = ((int64_t)blockIdx.x * WPB + wid) * 32;
-  if (k0 >= RN) return;
-  const int64_t k = k0 + lane;
-  const bool valid = k < RN;
-  const int64_t klast = k0 + 31 < RN ? k0 + 31 : RN - 1;
-  const int last_lane = (int)(klast - k0);
-  const uint32_t Nc32 = (uint32_t)P.Nc;
-  const int r_first = (int)((uint32_t)k0 / Nc32);
-  const bool one_run = r_first == (int)((uint32_t)klast / Nc32);
-  uint32_t st = 0, en = 0;
-  if (valid) {
-    st = k == 0 ? 0u : P.cell[k - 1];
-    en = P.cell[k];
-  }
-  const uint32_t S = __shfl_sync(FULL, st, 0);
-  const uint32_t E = __shfl_sync(FULL, en, last_lane);
-  const uint32_t cnt = E - S;
-  if (cnt > (uint32_t)capw) return;               // a k_collide_heavy tile
-  const int r = valid ? (int)((uint32_t)k / Nc32) : (int)((uint32_t)klast / Nc32);
-  const uint32_t c = valid ? (uint32_t)k - (uint32_t)r * Nc32 : 0u;
-  const uint32_t N = en - st, off = st - S;
-  const int h = P.ctl.parity[r];
-  const int reo = P.ctl.reorder[r];
-  const uint32_t rbase = run_lcr_base(P, r);
-  const int32_t s = *P.ctl.step;
-  int slot = -1;
-  if ((s + 1) % P.sample_every == 0 && (s + 1) / P.sample_every - 1 < P.n_slots) slot = (s + 1) / P.sample_every - 1;
-  const uint2 key = run_key(P, r);
-  uint32_t ncand = 0, nacc = 0;
-  float gm = valid ? P.gmax[k] : 0.0f;
-  const float gm0 = gm;
-  float* const wvx = reinterpret_cast<float*>(W.a);
-  // ---- load the contiguous slice (8 elements' loads per lane in flight)
-  const float* vsrc1 = reo ? (h ? P0 : P1) + 3 * RS + (int64_t)r * P.stride - rbase : P.stage;
-  for (uint32_t q0 = 0; q0 < cnt; q0 += 256) {
-    float vv[8][3];
-#pragma unroll
-    for (int u = 0; u < 8; u++) {
-      const uint32_t q = q0 + 32 * u + lane;
-      const float* vs = vsrc1;
-      if (q < cnt) {
-        const int64_t p = (int64_t)S + q;
-#pragma unroll
-        for (int a = 0; a < 3; a++) vv[u][a] = vs[a * RS + p];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 8; u++) {
-      const uint32_t q = q0 + 32 * u + lane;
-      if (q < cnt) { wvx[q] = vv[u][0]; W.vy[q] = vv[u][1]; W.vz[q] = vv[u][2]; W.mod[q] = 0; }
-    }
-  }
-  if (!one_run) {
-    // multi-run tile: per element, the view of its own run (rare: only run boundaries)
-    if (valid) for (uint32_t i = 0; i < N; i++) W.cell[off + i] = (uint8_t)lane;
-    __syncwarp();
-    for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
-      const uint32_t q = q0 + lane;
-      const int cq = q < cnt ? W.cell[q] : 0;
-      const int hq = __shfl_sync(FULL, h, cq), rq = __shfl_sync(FULL, reo, cq), runq = __shfl_sync(FULL, r, cq);
-      const uint32_t bq = __shfl_sync(FULL, rbase, cq);
-      if (q < cnt) {
-        const float* vs = rq ? (hq ? P0 : P1) + 3 * RS + (int64_t)runq * P.stride - bq : P.stage;
-        const int64_t p = (int64_t)S + q;
-        wvx[q] = vs[p];
-        W.vy[q] = vs[RS + p];
-        W.vz[q] = vs[2 * RS + p];
-      }
-    }
-  }
-  __syncwarp();
-  // ---- E: NTC (as in k_collide)
-  {
-    const uint32_t M = valid ? ntc_count(P, key, c, (uint32_t)s, N, gm) : 0u;
-    ncand = M;
-    uint32_t mst = M;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, mst, o); if (lane >= o) mst += y; }
-    const uint32_t tot = __shfl_sync(FULL, mst, 31);
-    mst -= M;
-    const double gmu = (double)gm, ghatu = gmu / P.sigma_c;
-    SmemCell Au{wvx + off, W.vy + off, W.vz + off, W.mod + off};
-    float maxg2 = 0.0f;
-    uint32_t naccu = 0;
-    for (uint32_t base = 0; base < tot; base += CCW) {
-      const uint32_t lim = tot - base < (uint32_t)CCW ? tot - base : (uint32_t)CCW;
-      for (uint32_t q0 = 0; q0 < lim; q0 += 64) {
-        uint32_t qq[2], kq[2], nc[2], cc[2];
-        int rc[2];
-#pragma unroll
-        for (int hh = 0; hh < 2; hh++) {
-          qq[hh] = q0 + 32 * hh + lane;
-          const uint32_t gq = base + qq[hh];
-          int lo = 0;
-#pragma unroll
-          for (int stp = 16; stp > 0; stp >>= 1) {
-            const uint32_t m = __shfl_sync(FULL, mst, lo + stp);
-            if (m <= gq && lo + stp < 32) lo += stp;
-          }
-          nc[hh] = __shfl_sync(FULL, N, lo);
-          kq[hh] = gq - __shfl_sync(FULL, mst, lo);
-          rc[hh] = __shfl_sync(FULL, r, lo);
-          cc[hh] = __shfl_sync(FULL, c, lo);
-        }
-        uint4 wp[2], wd[2];
-#pragma unroll
-        for (int hh = 0; hh < 2; hh++) {
-          const uint2 keyc = run_key(P, rc[hh]);
-          wp[hh] = draw(keyc, cc[hh], (uint32_t)s, TAG_COLL_PAIR, kq[hh], 0);
-          wd[hh] = draw(keyc, cc[hh], (uint32_t)s, TAG_COLL_DIR, kq[hh], 0);
-        }
-#pragma unroll
-        for (int hh = 0; hh < 2; hh++) {
-          const uint32_t q = qq[hh];
-          if (q < lim) {
-            const uint32_t i = lemire(wp[hh].x, nc[hh]);
-            uint32_t j = lemire(wp[hh].y, nc[hh] - 1);
-            if (j >= i) j++;
-            W.cij[q] = i | (j << 16);
-            W.cur[q] = wp[hh].z;
-            float pp = 2.0f * u_co(wd[hh].x) - 1.0f, qv = 2.0f * u_co(wd[hh].y) - 1.0f;
-            if (!(pp * pp + qv * qv < 1.0f)) {
-              pp = 2.0f * u_co(wd[hh].z) - 1.0f;
-              qv = 2.0f * u_co(wd[hh].w) - 1.0f;
-              if (!(pp * pp + qv * qv < 1.0f))
-                marsaglia_pq_from(run_key(P, rc[hh]), cc[hh], (uint32_t)s, kq[hh], 1, pp, qv);
-            }
-            W.cp[q] = pp;
-            W.cq[q] = qv;
-          }
-        }
-      }
-      __syncwarp();
-      if (M) {
-        const uint32_t a0 = mst > base ? mst : base;
-        const uint32_t a1 = mst + M < base + lim ? mst + M : base + lim;
-        if (a0 < a1)
-          ntc_apply(P, Au, gmu, ghatu, W.cij + (a0 - base), W.cur + (a0 - base), W.cp + (a0 - base),
-                    W.cq + (a0 - base), a1 - a0, maxg2, naccu);
-      }
-      __syncwarp();
-    }
-    if (valid && M) {
-      nacc = naccu;
-      const double sgm = P.model == 0 ? P.sigma_c * sqrt((double)maxg2) : P.sigma_c * pow((double)maxg2, P.omega1);
-      if (sgm > (double)gm) gm = (float)sgm;
-    }
-  }
-  if (valid && slot >= 0) sample_cell(P, slot, k, N, SmemCell{wvx + off, W.vy + off, W.vz + off, W.mod + off});
-  __syncwarp();
-  // ---- F: write back the particles that collided
-  for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
-    const uint32_t q = q0 + lane;
-    int hq = h, rq = reo, runq = r;
-    uint32_t bq = rbase;
-    if (!one_run) {
-      const int cq = q < cnt ? W.cell[q] : 0;
-      hq = __shfl_sync(FULL, h, cq); rq = __shfl_sync(FULL, reo, cq); runq = __shfl_sync(FULL, r, cq);
-      bq = __shfl_sync(FULL, rbase, cq);
-    }
-    if (q < cnt && W.mod[q]) {
-      float* d;
-      if (rq) d = (hq ? P0 : P1) + 3 * RS + (int64_t)runq * P.stride - bq + ((int64_t)S + q);
-      else d = (hq ? P1 : P0) + 3 * RS + P.lcr[S + q];
-      d[0] = wvx[q];
-      d[RS] = W.vy[q];
-      d[2 * RS] = W.vz[q];
-    }
-  }
-  if (valid && gm != gm0) P.gmax[k] = gm;
-  if (valid && P.debug) { P.dbg_cand[k] = ncand; P.dbg_acc[k] = (int32_t)nacc; }
-  const uint32_t rk = valid ? (uint32_t)r : 0xFFFFFFFFu;
-  const unsigned m = __match_any_sync(FULL, rk);
-  const uint32_t sc = __reduce_add_sync(m, ncand), sa = __reduce_add_sync(m, nacc);
-  if (valid && lane == __ffs(m) - 1 && sc) {
-    atomicAdd(&P.ctl.counters[r * 4 + 2], (unsigned long long)sc);
-    atomicAdd(&P.ctl.counters[r * 4 + 3], (unsigned long long)sa);
-  }
-}
-
-// ---------------------------------------------------------------------------
 // k_collide_heavy: the warp tiles k_collide could not stage (dense cells, e.g.
 // c5's orifice jet).  The GPU analog of TLPDPR's processor heap (PAPER.md
 // 501-515, Eq. 12): a persistent block "borrows" 256 threads and a large
@@ -2050,28 +1699,6 @@ static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t s
   k_collide<D, NET><<<g, WPB * 32, smem, st>>>(P, mode, slot, capw);
 }
 
-template <int D, int NET>
-static void split_t(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
-  const int64_t RN = (int64_t)P.R * P.Nc;
-  const int64_t warps = (RN + 31) / 32;
-  const size_t s1 = SWPB * stage_smem_bytes(P.capw), s2 = WPB * warp_smem_bytes(P.capw);
-  static size_t c1 = 0, c2 = 0;
-  if (s1 > c1) { cudaFuncSetAttribute(k_stage<D, NET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1); c1 = s1; }
-  if (s2 > c2) { cudaFuncSetAttribute(k_ntc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2); c2 = s2; }
-  hook.before(KSLOT_STAGE);
-  k_stage<D, NET><<<(unsigned)((warps + SWPB - 1) / SWPB), SWPB * 32, s1, st>>>(P, P.capw);
-  hook.after(KSLOT_STAGE);
-  hook.before(KSLOT_COLLIDE);
-  k_ntc<D><<<(unsigned)((warps + WPB - 1) / WPB), WPB * 32, s2, st>>>(P, P.capw);
-  hook.after(KSLOT_COLLIDE);
-}
-
-void launch_split(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
-  if (P.dim == 1) { if (P.net_wide) split_t<1, 32>(P, st, hook); else split_t<1, 16>(P, st, hook); }
-  else if (P.dim == 2) { if (P.net_wide) split_t<2, 32>(P, st, hook); else split_t<2, 16>(P, st, hook); }
-  else { if (P.net_wide) split_t<3, 32>(P, st, hook); else split_t<3, 16>(P, st, hook); }
-}
-
 void launch_collide(const Prm& P, int mode, int slot, cudaStream_t st) {
   // register sorting network width: 16 for sparse cells, 32 for dense ones
   const bool wide = P.net_wide != 0;
@@ -2132,13 +1759,9 @@ void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
   hook.before(KSLOT_SCATTER);
   launch_scatter(P, st);
   hook.after(KSLOT_SCATTER);
-  if (P.stage) {
-    launch_split(P, st, hook);
-  } else {
-    hook.before(KSLOT_COLLIDE);
-    launch_collide(P, 0, -1, st);
-    hook.after(KSLOT_COLLIDE);
-  }
+  hook.before(KSLOT_COLLIDE);
+  launch_collide(P, 0, -1, st);
+  hook.after(KSLOT_COLLIDE);
   hook.before(KSLOT_COLLIDE_HEAVY);
   launch_collide_heavy(P, 0, -1, st);
   hook.after(KSLOT_COLLIDE_HEAVY);
@@ -2170,7 +1793,6 @@ const char* kernel_slot_name(int k) {
     case KSLOT_SCATTER: return "k_scatter";
     case KSLOT_COLLIDE: return "k_collide";
     case KSLOT_COLLIDE_HEAVY: return "k_collide_heavy";
-    case KSLOT_STAGE: return "k_stage";
     case KSLOT_STEP_END: return "k_step_end";
     default: return "";
   }

@@ -20,7 +20,6 @@ enum KernelSlot {
   KSLOT_COLLIDE,
   KSLOT_STEP_END,
   KSLOT_COLLIDE_HEAVY,
-  KSLOT_STAGE,
   KSLOT_COUNT
 };
 
