@@ -594,25 +594,25 @@ __global__ void __launch_bounds__(256) k_scatter(Prm P) {
     if (ibase >= n) continue;
     const int64_t base = (int64_t)r * P.stride;
     const uint32_t* K = P.key + base;
-    for (int64_t i0w = ibase + (threadIdx.x >> 5) * 256; i0w < ibase + ITEM && i0w < n; i0w += 2048) {
-      uint32_t kk[8], m[8], p0[8];
+    for (int64_t i0w = ibase + (threadIdx.x >> 5) * 128; i0w < ibase + ITEM && i0w < n; i0w += 1024) {
+    uint32_t kk[4], m[4], p0[4];
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const int64_t i = i0w + j * 32 + lane;
-        kk[j] = i < n ? K[i] : DEAD_KEY;
-      }
+    for (int j = 0; j < 4; j++) {
+      const int64_t i = i0w + j * 32 + lane;
+      kk[j] = i < n ? K[i] : DEAD_KEY;
+    }
 #pragma unroll
-      for (int j = 0; j < 8; j++) m[j] = __match_any_sync(FULL, kk[j]);
+    for (int j = 0; j < 4; j++) m[j] = __match_any_sync(FULL, kk[j]);
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        p0[j] = 0;
-        if (kk[j] != DEAD_KEY && lane == __ffs(m[j]) - 1) p0[j] = atomicAdd(&P.cell[kk[j]], (uint32_t)__popc(m[j]));
-      }
+    for (int j = 0; j < 4; j++) {
+      p0[j] = 0;
+      if (kk[j] != DEAD_KEY && lane == __ffs(m[j]) - 1) p0[j] = atomicAdd(&P.cell[kk[j]], (uint32_t)__popc(m[j]));
+    }
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const uint32_t b = __shfl_sync(FULL, p0[j], __ffs(m[j]) - 1);
-        if (kk[j] != DEAD_KEY) P.lcr[b + __popc(m[j] & lt)] = (uint32_t)(base + i0w + j * 32 + lane);
-      }
+    for (int j = 0; j < 4; j++) {
+      const uint32_t b = __shfl_sync(FULL, p0[j], __ffs(m[j]) - 1);
+      if (kk[j] != DEAD_KEY) P.lcr[b + __popc(m[j] & lt)] = (uint32_t)(base + i0w + j * 32 + lane);
+    }
     }
   }
   queue_done(P.ctl.queue + 2);
