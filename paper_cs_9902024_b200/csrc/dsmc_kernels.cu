@@ -479,19 +479,6 @@ __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
   const uint2 key = run_key(P, r);
   const uint32_t kbase = (uint32_t)r * (uint32_t)P.Nc;
   uint32_t removed = 0;
-  // the in-cell ranks of chunk t-1 are resolved after chunk t's loads are in
-  // flight, so the returning histogram atomics overlap the memory latency
-  bool pend = false;
-  unsigned pm[4] = {0, 0, 0, 0};
-  uint32_t pp0[4] = {0, 0, 0, 0}, pk[4] = {0, 0, 0, 0};
-  int64_t pi0 = 0;
-  auto resolve = [&]() {
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const uint32_t b = __shfl_sync(FULL, pp0[j], __ffs(pm[j]) - 1);
-      if (pk[j] != DEAD_KEY) RK[pi0 + j * 32 + lane] = b + __popc(pm[j] & ((1u << lane) - 1u));
-    }
-  };
   for (int64_t i0w = ibase + (threadIdx.x >> 5) * 128; i0w < ibase + ITEM && i0w < n; i0w += 1024) {
     float x[4][3], v[4][3];
 #pragma unroll
@@ -505,7 +492,6 @@ __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
 #pragma unroll
       for (int a = 0; a < 3; a++) v[j][a] = in ? V[a][i] : 0.0f;
     }
-    if (pend) resolve();
     uint32_t kk[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
@@ -535,18 +521,23 @@ __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
       if (i < n) K[i] = kk[j];
     }
     // warp-aggregated counts; the returned old count gives each particle its
-    // rank inside its cell (so k_scatter needs no atomics)
+    // rank inside its cell (used by k_scatter, so that pass needs no atomics)
+    unsigned mm[4];
+    uint32_t p0[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) mm[j] = __match_any_sync(FULL, kk[j]);
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      pm[j] = __match_any_sync(FULL, kk[j]);
-      pk[j] = kk[j];
-      pp0[j] = 0;
-      if (kk[j] != DEAD_KEY && lane == __ffs(pm[j]) - 1) pp0[j] = atomicAdd(&P.cell[kk[j]], (uint32_t)__popc(pm[j]));
+      p0[j] = 0;
+      if (kk[j] != DEAD_KEY && lane == __ffs(mm[j]) - 1) p0[j] = atomicAdd(&P.cell[kk[j]], (uint32_t)__popc(mm[j]));
     }
-    pi0 = i0w;
-    pend = true;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const uint32_t b = __shfl_sync(FULL, p0[j], __ffs(mm[j]) - 1);
+      const int64_t i = i0w + j * 32 + lane;
+      if (kk[j] != DEAD_KEY) RK[i] = b + __popc(mm[j] & ((1u << lane) - 1u));
+    }
   }
-  if (pend) resolve();
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) removed += __shfl_xor_sync(FULL, removed, o);
   if (lane == 0 && removed) atomicAdd(&P.ctl.counters[r * 4 + 1], (unsigned long long)removed);
