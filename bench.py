@@ -118,10 +118,10 @@ def algorithmic_bytes(p, kernel, live, cells, accepted, sample, reorder):
     """Bytes a kernel must move per launch.
     live: live particles of the batch, cells: n*Nc, accepted: pairs this step."""
     D = p["dim"]
-    if kernel == "k_motion":      # R pos(4D)+vel(12), W pos(4D), W key(4), W rank(4); counts 4/cell
-        return live * (8 * D + 20) + 4 * cells
-    if kernel == "k_scatter":     # R key 4 + rank 4, W LCR 4; starts R 4/cell
-        return live * 12 + 4 * cells
+    if kernel == "k_motion":      # R pos(4D)+vel(12), W pos(4D), W key(4); counts 4/cell
+        return live * (8 * D + 16) + 4 * cells
+    if kernel == "k_scatter":     # R key 4, W LCR 4; cursor R+W 8/cell
+        return live * 8 + 8 * cells
     if kernel == "k_collide":     # R ends 4 + gmax 4 /cell, R LCR 4 + vel 12, W vel of collided
         b = live * 16 + 8 * cells + 2 * accepted * 12
         if sample:

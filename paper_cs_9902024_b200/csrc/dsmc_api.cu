@@ -44,7 +44,7 @@ struct Layout {
   // ctl offsets
   size_t c_step, c_status, c_nstore, c_parity, c_reorder, c_inserted, c_counters, c_live, c_psteps, c_slot, c_queue, c_heavy;
   // scratch offsets
-  size_t s_face_j, s_face_k, s_open, s_kept, s_part, s_macros, s_heavy, s_rank, s_cand, s_acc;
+  size_t s_face_j, s_face_k, s_open, s_kept, s_part, s_macros, s_heavy, s_cand, s_acc;
 };
 
 // face-cell lists of the x- face (reading R8)
@@ -130,7 +130,7 @@ int make_layout(const dsmc_problem* p, int debug, Layout& L) {
   s.P = 2 * 6 * slots * sizeof(float);
   s.key = slots * sizeof(uint32_t);
   s.lcr = slots * sizeof(uint32_t);
-  s.cell = align_up(((size_t)L.RN + 1) * sizeof(uint32_t), 16);
+  s.cell = align_up((size_t)L.RN * sizeof(uint32_t), 16);
   s.gmax = (size_t)L.RN * sizeof(float);
   s.C = (size_t)s.n_slots * 5 * (size_t)L.RN * sizeof(double);
   if (s.C == 0) s.C = 8;
@@ -156,11 +156,10 @@ int make_layout(const dsmc_problem* p, int debug, Layout& L) {
   L.s_face_k = o; o = align_up(o + 4 * F, 256);
   L.s_open = o; o = align_up(o + F, 256);
   L.s_kept = o; o = align_up(o + 4 * R * (size_t)(L.n_face > 0 ? L.n_face : 1), 256);
-  const int64_t Lscan = (L.RN > L.Nc ? L.RN : L.Nc) + 1;
+  const int64_t Lscan = L.RN > L.Nc ? L.RN : L.Nc;
   L.s_part = o; o = align_up(o + 4 * ((size_t)dsmc::scan_tiles(Lscan) + 1), 256);
   L.s_macros = o; o = align_up(o + 8 * 10 * (size_t)L.Nc, 256);
   L.s_heavy = o; o = align_up(o + 4 * ((size_t)(L.RN + 31) / 32 + 1), 256);
-  L.s_rank = o; o = align_up(o + 4 * (size_t)p->n_runs * (size_t)L.stride, 256);
   if (debug) {
     L.s_cand = o; o = align_up(o + 8 * (size_t)L.RN, 256);
     L.s_acc = o; o = align_up(o + 4 * (size_t)L.RN, 256);
@@ -332,7 +331,6 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   P.ctl.queue = (unsigned long long*)(ct + L.c_queue);
   P.ctl.heavy = (uint32_t*)(ct + L.c_heavy);
   P.heavy_list = (uint32_t*)(sc + L.s_heavy);
-  P.rank = (uint32_t*)(sc + L.s_rank);
   P.caph = 8192;
 
   auto bail = [&](int code) { delete c; return code; };
@@ -612,16 +610,21 @@ int dsmc_get_index(dsmc_ctx* c, int32_t run, int64_t* live_out, int64_t* count, 
   if (!c || !live_out || run < 0 || run >= c->prob.n_runs) return fail(DSMC_EINVAL, "bad argument");
   if (!c->debug) return fail(DSMC_EINVAL, "get_index needs a debug context");
   const int64_t Nc = c->L.Nc;
-  std::vector<uint32_t> starts((size_t)Nc + 1);
+  std::vector<uint32_t> ends((size_t)Nc + 1);
   const int64_t k0 = (int64_t)run * Nc;
-  CK(cudaMemcpyAsync(starts.data(), c->P.cell + k0, 4 * ((size_t)Nc + 1), cudaMemcpyDeviceToHost, c->stream));
+  if (run == 0) {
+    ends[0] = 0;
+    CK(cudaMemcpyAsync(ends.data() + 1, c->P.cell, 4 * (size_t)Nc, cudaMemcpyDeviceToHost, c->stream));
+  } else {
+    CK(cudaMemcpyAsync(ends.data(), c->P.cell + k0 - 1, 4 * ((size_t)Nc + 1), cudaMemcpyDeviceToHost, c->stream));
+  }
   CK(cudaStreamSynchronize(c->stream));
-  const uint32_t base = starts[0];
-  const int64_t live = (int64_t)(starts[Nc] - base);
+  const uint32_t base = ends[0];
+  const int64_t live = (int64_t)(ends[Nc] - base);
   *live_out = live;
   for (int64_t q = 0; q < Nc; q++) {
-    if (count) count[q] = (int64_t)(starts[q + 1] - starts[q]);
-    if (start) start[q] = (int64_t)(starts[q] - base);
+    if (count) count[q] = (int64_t)(ends[q + 1] - ends[q]);
+    if (start) start[q] = (int64_t)(ends[q] - base);
   }
   if (lcr && live) {
     std::vector<uint32_t> g((size_t)live);

@@ -82,9 +82,8 @@ struct Prm {
   // buffers
   float* P;                  // [2][6][R*stride]
   uint32_t* key;             // [R*stride]
-  uint32_t* rank;            // [R*stride] rank of the particle inside its cell (this step)
   uint32_t* lcr;             // [R*stride]
-  uint32_t* cell;            // [R*Nc + 1] counts -> exclusive starts (total last)
+  uint32_t* cell;            // [R*Nc]
   float* gmax;               // [R*Nc]
   double* C;                 // [n_slots][5][R*Nc]
   uint32_t* scan_part;       // scan tile partials

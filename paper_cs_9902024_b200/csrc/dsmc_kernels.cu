@@ -300,7 +300,7 @@ __global__ void k_inflow_emit(Prm P) {
         }
         const uint32_t kk = (uint32_t)r * (uint32_t)P.Nc + (uint32_t)(ic[0] + P.nx * (ic[1] + P.ny * ic[2]));
         P.key[base + i] = kk;
-        P.rank[base + i] = atomicAdd(&P.cell[kk], 1u);
+        atomicAdd(&P.cell[kk], 1u);
       } else {
         latch(P, ST_CAP);
       }
@@ -475,7 +475,6 @@ __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
 #pragma unroll
   for (int a = 0; a < 3; a++) { X[a] = parr(P, h, a) + base; V[a] = parr(P, h, 3 + a) + base; }
   uint32_t* K = P.key + base;
-  uint32_t* RK = P.rank + base;
   const uint2 key = run_key(P, r);
   const uint32_t kbase = (uint32_t)r * (uint32_t)P.Nc;
   uint32_t removed = 0;
@@ -520,22 +519,11 @@ __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
       }
       if (i < n) K[i] = kk[j];
     }
-    // warp-aggregated counts; the returned old count gives each particle its
-    // rank inside its cell (used by k_scatter, so that pass needs no atomics)
-    unsigned mm[4];
-    uint32_t p0[4];
-#pragma unroll
-    for (int j = 0; j < 4; j++) mm[j] = __match_any_sync(FULL, kk[j]);
+    // warp-aggregated histogram of cell keys
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      p0[j] = 0;
-      if (kk[j] != DEAD_KEY && lane == __ffs(mm[j]) - 1) p0[j] = atomicAdd(&P.cell[kk[j]], (uint32_t)__popc(mm[j]));
-    }
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const uint32_t b = __shfl_sync(FULL, p0[j], __ffs(mm[j]) - 1);
-      const int64_t i = i0w + j * 32 + lane;
-      if (kk[j] != DEAD_KEY) RK[i] = b + __popc(mm[j] & ((1u << lane) - 1u));
+      const unsigned m = __match_any_sync(FULL, kk[j]);
+      if (kk[j] != DEAD_KEY && lane == __ffs(m) - 1) atomicAdd(&P.cell[kk[j]], (uint32_t)__popc(m));
     }
   }
 #pragma unroll
@@ -559,7 +547,7 @@ __global__ void k_step_mid(Prm P) {
 }
 
 __device__ __forceinline__ uint32_t run_lcr_base(const Prm& P, int r) {
-  return P.cell[(int64_t)r * P.Nc];
+  return r == 0 ? 0u : P.cell[(int64_t)r * P.Nc - 1];
 }
 
 __global__ void k_step_end(Prm P, int mode, int slot) {
@@ -572,7 +560,7 @@ __global__ void k_step_end(Prm P, int mode, int slot) {
   const int32_t s = *P.ctl.step;
   if (r < P.R) {
     const uint32_t b = run_lcr_base(P, r);
-    const uint32_t e = P.cell[(int64_t)(r + 1) * P.Nc];
+    const uint32_t e = P.cell[(int64_t)(r + 1) * P.Nc - 1];
     P.ctl.live[r] = (int64_t)(e - b);
     if (P.ctl.reorder[r]) {
       P.ctl.n_store[r] = (int64_t)(e - b);
@@ -594,6 +582,7 @@ __global__ void k_step_end(Prm P, int mode, int slot) {
 // a chunk are issued before any result is consumed.
 __global__ void __launch_bounds__(256) k_scatter(Prm P) {
   const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
   const int64_t items_per_run = (P.cap + ITEM - 1) / ITEM;
   const int64_t n_items = items_per_run * P.R;
   __shared__ int64_t s_item;
@@ -605,20 +594,25 @@ __global__ void __launch_bounds__(256) k_scatter(Prm P) {
     if (ibase >= n) continue;
     const int64_t base = (int64_t)r * P.stride;
     const uint32_t* K = P.key + base;
-    const uint32_t* RK = P.rank + base;
     for (int64_t i0w = ibase + (threadIdx.x >> 5) * 128; i0w < ibase + ITEM && i0w < n; i0w += 1024) {
-      uint32_t kk[4], rk[4], st[4];
+    uint32_t kk[4], m[4], p0[4];
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const int64_t i = i0w + j * 32 + lane;
-        kk[j] = i < n ? K[i] : DEAD_KEY;
-        rk[j] = i < n ? RK[i] : 0u;
-      }
+    for (int j = 0; j < 4; j++) {
+      const int64_t i = i0w + j * 32 + lane;
+      kk[j] = i < n ? K[i] : DEAD_KEY;
+    }
 #pragma unroll
-      for (int j = 0; j < 4; j++) st[j] = kk[j] != DEAD_KEY ? P.cell[kk[j]] : 0u;
+    for (int j = 0; j < 4; j++) m[j] = __match_any_sync(FULL, kk[j]);
 #pragma unroll
-      for (int j = 0; j < 4; j++)
-        if (kk[j] != DEAD_KEY) P.lcr[st[j] + rk[j]] = (uint32_t)(base + i0w + j * 32 + lane);
+    for (int j = 0; j < 4; j++) {
+      p0[j] = 0;
+      if (kk[j] != DEAD_KEY && lane == __ffs(m[j]) - 1) p0[j] = atomicAdd(&P.cell[kk[j]], (uint32_t)__popc(m[j]));
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const uint32_t b = __shfl_sync(FULL, p0[j], __ffs(m[j]) - 1);
+      if (kk[j] != DEAD_KEY) P.lcr[b + __popc(m[j] & lt)] = (uint32_t)(base + i0w + j * 32 + lane);
+    }
     }
   }
   queue_done(P.ctl.queue + 2);
@@ -930,8 +924,8 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
   // ---- A
   uint32_t st = 0, en = 0;
   if (valid) {
-    st = P.cell[k];
-    en = P.cell[k + 1];
+    st = k == 0 ? 0u : P.cell[k - 1];
+    en = P.cell[k];
   }
   const int r = valid ? (int)((uint32_t)k / Nc32) : r_last;
   const uint32_t c = valid ? (uint32_t)k - (uint32_t)r * Nc32 : 0u;
@@ -1313,8 +1307,8 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
       const int64_t k = k0 + t;
       uint32_t st = 0, en = 0;
       if (valid) {
-        st = P.cell[k];
-        en = P.cell[k + 1];
+        st = k == 0 ? 0u : P.cell[k - 1];
+        en = P.cell[k];
         r = (int)((uint32_t)k / Nc32);
         c = (uint32_t)k - (uint32_t)r * Nc32;
         h = P.ctl.parity[r];
@@ -1752,7 +1746,7 @@ void launch_selftest_philox(int64_t n, const uint32_t* ctr, uint32_t k0, uint32_
 // one full step: kernel order of PAPER.md Fig. 1
 void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
   hook.before(KSLOT_ZERO);
-  launch_zero(P.cell, (int64_t)P.R * P.Nc + 1, st);
+  launch_zero(P.cell, (int64_t)P.R * P.Nc, st);
   hook.after(KSLOT_ZERO);
   launch_inflow(P, st, hook);
   hook.before(KSLOT_MOTION);
@@ -1761,7 +1755,7 @@ void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
   hook.before(KSLOT_STEP_MID);
   launch_step_mid(P, st);
   hook.after(KSLOT_STEP_MID);
-  launch_scan(P.cell, (int64_t)P.R * P.Nc + 1, P.scan_part, st, hook);   // starts, total at [R*Nc]
+  launch_scan(P.cell, (int64_t)P.R * P.Nc, P.scan_part, st, hook);
   hook.before(KSLOT_SCATTER);
   launch_scatter(P, st);
   hook.after(KSLOT_SCATTER);
@@ -1777,9 +1771,9 @@ void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
 }
 
 void issue_sample(const Prm& P, int slot, cudaStream_t st) {
-  launch_zero(P.cell, (int64_t)P.R * P.Nc + 1, st);
+  launch_zero(P.cell, (int64_t)P.R * P.Nc, st);
   launch_motion(P, 1, st);
-  launch_scan(P.cell, (int64_t)P.R * P.Nc + 1, P.scan_part, st, LaunchHook{});
+  launch_scan(P.cell, (int64_t)P.R * P.Nc, P.scan_part, st, LaunchHook{});
   launch_scatter(P, st);
   launch_collide(P, 1, slot, st);
   launch_collide_heavy(P, 1, slot, st);
