@@ -997,11 +997,22 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
     // ---- D
     float* const wvx = reinterpret_cast<float*>(W.a);
     if (one_run) {
+      // per-array base pointers indexed by 32-bit offsets (one IMAD.WIDE per access)
       const float* __restrict__ sx = (h ? P1 : P0) + 3 * RS;
+      const float* __restrict__ sy = sx + RS;
+      const float* __restrict__ sz = sy + RS;
+      {  // clear the collided flags with word stores
+        uint32_t* m32 = reinterpret_cast<uint32_t*>(W.mod);
+        for (uint32_t w = lane; w < (cnt + 3) / 4; w += 32) m32[w] = 0u;
+      }
       // gathers batched per lane (4 or 8 elements' loads issued before any store)
       if (reo) {
         const float* __restrict__ px = (h ? P1 : P0);
+        const float* __restrict__ py = px + RS;
+        const float* __restrict__ pz = py + RS;
         float* __restrict__ dx = (h ? P0 : P1) + (int64_t)r * P.stride + (S - rbase);
+        float* __restrict__ dy = dx + RS;
+        float* __restrict__ dz = dy + RS;
         for (uint32_t q0 = 0; q0 < cnt; q0 += 128) {
           uint32_t gg[4];
           float xs[4][D], vv[4][3];
@@ -1013,10 +1024,12 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
 #pragma unroll
           for (int u = 0; u < 4; u++) {
             if (q0 + 32 * u + lane < cnt) {
-#pragma unroll
-              for (int a = 0; a < D; a++) xs[u][a] = px[a * RS + gg[u]];
-#pragma unroll
-              for (int a = 0; a < 3; a++) vv[u][a] = sx[a * RS + gg[u]];
+              xs[u][0] = px[gg[u]];
+              if (D > 1) xs[u][D > 1 ? 1 : 0] = py[gg[u]];
+              if (D > 2) xs[u][D > 2 ? 2 : 0] = pz[gg[u]];
+              vv[u][0] = sx[gg[u]];
+              vv[u][1] = sy[gg[u]];
+              vv[u][2] = sz[gg[u]];
             }
           }
 #pragma unroll
@@ -1026,9 +1039,9 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
               wvx[q] = vv[u][0];
               W.vy[q] = vv[u][1];
               W.vz[q] = vv[u][2];
-              W.mod[q] = 0;
-#pragma unroll
-              for (int a = 0; a < D; a++) dx[a * RS + q] = xs[u][a];
+              dx[q] = xs[u][0];
+              if (D > 1) dy[q] = xs[u][D > 1 ? 1 : 0];
+              if (D > 2) dz[q] = xs[u][D > 2 ? 2 : 0];
             }
           }
         }
@@ -1044,8 +1057,9 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
 #pragma unroll
           for (int u = 0; u < 8; u++) {
             if (q0 + 32 * u + lane < cnt) {
-#pragma unroll
-              for (int a = 0; a < 3; a++) vv[u][a] = sx[a * RS + gg[u]];
+              vv[u][0] = sx[gg[u]];
+              vv[u][1] = sy[gg[u]];
+              vv[u][2] = sz[gg[u]];
             }
           }
 #pragma unroll
@@ -1055,7 +1069,6 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
               wvx[q] = vv[u][0];
               W.vy[q] = vv[u][1];
               W.vz[q] = vv[u][2];
-              W.mod[q] = 0;
             }
           }
         }
@@ -1170,19 +1183,23 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
     if (one_run) {
       if (reo) {
         float* __restrict__ dx = (h ? P0 : P1) + 3 * RS + (int64_t)r * P.stride + (S - rbase);
+        float* __restrict__ dy = dx + RS;
+        float* __restrict__ dz = dy + RS;
         for (uint32_t q = lane; q < cnt; q += 32) {
           dx[q] = wvx[q];
-          dx[RS + q] = W.vy[q];
-          dx[2 * RS + q] = W.vz[q];
+          dy[q] = W.vy[q];
+          dz[q] = W.vz[q];
         }
       } else {
         float* __restrict__ vxp = (h ? P1 : P0) + 3 * RS;
+        float* __restrict__ vyp = vxp + RS;
+        float* __restrict__ vzp = vyp + RS;
         for (uint32_t q = lane; q < cnt; q += 32) {
           if (W.mod[q]) {
             const uint32_t g = W.sorted[q];
             vxp[g] = wvx[q];
-            vxp[RS + g] = W.vy[q];
-            vxp[2 * RS + g] = W.vz[q];
+            vyp[g] = W.vy[q];
+            vzp[g] = W.vz[q];
           }
         }
       }
@@ -1278,7 +1295,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
   __shared__ uint32_t s_wmax;
   __shared__ int c_r[32], c_h[32], c_reo[32];
   __shared__ float c_gm[32];
-  __shared__ uint32_t s_tile, s_warp[HT / 32];
+  __shared__ uint32_t s_tile;
   const int t = threadIdx.x;
   const int64_t RN = (int64_t)P.R * P.Nc;
   const int64_t RS = (int64_t)P.R * P.stride;
