@@ -42,7 +42,7 @@ def find(m):
 kstart = find("k_collide(Prm P, int mode, int slot_arg, int capw) {")
 marks = [("A", kstart), ("B", find("    // ---- B")), ("C", find("    // ---- C")), ("D", find("    // ---- D")),
          ("E0", find("    // ---- E")), ("E1", find("      for (uint32_t base = 0; base < tot; base += CCW) {")),
-         ("E2", find("        if (Mu) {")), ("Efin", find("      W.mg2[u] = maxg2;")),
+         ("E2", find("        if (Mu) {")), ("Efin", find("      if (valid && M) {")),
          ("F", find("    // ---- F")), ("G", find("tile too large for the warp")),
          ("end", find("// per-run counters: aggregate") + 12)]
 fns = [("marsaglia_pq", find("__device__ __forceinline__ void marsaglia_pq")),
