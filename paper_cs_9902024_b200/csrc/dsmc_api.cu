@@ -4,6 +4,7 @@
 // kernels of dsmc_kernels.cu; there is no CPU fallback.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -285,8 +286,11 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
     int32_t ppc_max = 0;
     for (int k = 0; k < p->n_fill; k++) ppc_max = p->fill[k].ppc > ppc_max ? p->fill[k].ppc : ppc_max;
     if (p->inflow_kind == DSMC_INFLOW_GHOST) ppc_max = std::max(ppc_max, (int32_t)std::ceil(p->inflow_n));
-    int32_t capw = 32 * ppc_max + 8 * (int32_t)std::ceil(std::sqrt(32.0 * ppc_max)) + 64;
+    // (5 sigma of the Poisson tile count: 4 blocks of 4 warps then stay under the
+    // 196 KB shared-memory carveout, which leaves the L1 the gathers need)
+    int32_t capw = 32 * ppc_max + 5 * (int32_t)std::ceil(std::sqrt(32.0 * ppc_max)) + 32;
     capw = std::max(256, std::min(capw, 4096));
+    if (const char* e = std::getenv("DSMC_CAPW")) capw = std::max(256, std::min(std::atoi(e), 4096));   // A/B experiments
     P.capw = (capw + 31) / 32 * 32;
   }
   P.n_fill = p->n_fill;

@@ -19,6 +19,7 @@
 // within-cell order (ascending store index, reading R11) is restored inside
 // k_collide, which stages each tile of cells in shared memory.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <curand_kernel.h>
 
@@ -793,25 +794,72 @@ __device__ __forceinline__ void ntc_apply(const Prm& P, const A& acc, double gm,
   }
 }
 
-// in-register bitonic sorting network (ascending), NN a power of two
-template <int NN>
-__device__ __forceinline__ void sort_net(uint32_t (&a)[NN]) {
+// candidates of one cell in increasing k with everything velocity-independent
+// drawn ahead (k_collide): ij = i | j << 16; thr = HS threshold F (accept iff
+// g2 > F) or the raw VHS acceptance word; (ex, ey, ez) the unit vector (R14)
+template <class A>
+__device__ __forceinline__ void ntc_apply_pre(const Prm& P, const A& acc, double gm, const uint32_t* ij,
+                                              const uint32_t* thr, const float* ex, const float* ey, const float* ez,
+                                              uint32_t n, float& maxg2, uint32_t& nacc) {
+  for (uint32_t k = 0; k < n; k++) {
+    const uint32_t pr = ij[k];
+    const uint32_t i = pr & 0xFFFFu, j = pr >> 16;
+    float a[3], b[3];
+    acc.ld(i, a);
+    acc.ld(j, b);
+    const float dx = a[0] - b[0], dy = a[1] - b[1], dz = a[2] - b[2];
+    const float g2 = (dx * dx + dy * dy) + dz * dz;
+    maxg2 = g2 > maxg2 ? g2 : maxg2;
+    const bool accept = P.model == 0 ? g2 > __uint_as_float(thr[k])
+                                     : u_co_d(thr[k]) * gm < P.sigma_c * pow((double)g2, P.omega1);
+    if (accept) {
+      const float e[3] = {ex[k], ey[k], ez[k]};
+      const float cmx = (a[0] + b[0]) * 0.5f, cmy = (a[1] + b[1]) * 0.5f, cmz = (a[2] + b[2]) * 0.5f;
+      const float hh = 0.5f * sqrtf(g2);
+      const float pa[3] = {cmx + hh * e[0], cmy + hh * e[1], cmz + hh * e[2]};
+      const float pb[3] = {cmx - hh * e[0], cmy - hh * e[1], cmz - hh * e[2]};
+      acc.st(i, pa);
+      acc.st(j, pb);
+      nacc++;
+    }
+  }
+}
+
+// odd-even merge sorting network (Batcher) over the first NE <= NN entries,
+// ascending; NN a power of two.  Comparators reaching past NE are dropped:
+// with the tail padded by +inf they never swap (0-1 principle; exhaustively
+// checked by tests/test_sortnet.py).
+template <int NN, int NE>
+__host__ __device__ __forceinline__ void sort_oem(uint32_t (&a)[NN]) {
+  // stage (p, k) compares x with x + k for every x with (x - k%p) mod 2k < k
+  // inside one 2p-block; every loop bound is a constant, so the network
+  // unrolls completely and a[] stays in registers
 #pragma unroll
-  for (int k = 2; k <= NN; k <<= 1) {
+  for (int p = 1; p < NN; p <<= 1) {
 #pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
+    for (int k = p; k >= 1; k >>= 1) {
 #pragma unroll
-      for (int i = 0; i < NN; i++) {
-        const int l = i ^ j;
-        if (l > i) {
-          const uint32_t x = a[i], y = a[l];
-          const bool asc = (i & k) == 0;
-          a[i] = asc ? min(x, y) : max(x, y);
-          a[l] = asc ? max(x, y) : min(x, y);
+      for (int x = 0; x < NN; x++) {
+        const int j0 = k % p;
+        if (x >= j0 && (x - j0) % (2 * k) < k && x + k < NE && x / (2 * p) == (x + k) / (2 * p)) {
+          const uint32_t u = a[x], v = a[x + k];
+          a[x] = u < v ? u : v;
+          a[x + k] = u < v ? v : u;
         }
       }
     }
   }
+}
+
+// sort a segment of N <= NE from src into dst (shared memory), in registers
+template <int NN, int NE>
+__device__ __forceinline__ void sort_segment(const uint32_t* src, uint32_t* dst, uint32_t N) {
+  uint32_t v[NN];
+#pragma unroll
+  for (int i = 0; i < NN; i++) v[i] = (i < NE && (uint32_t)i < N) ? src[i] : 0xFFFFFFFFu;
+  sort_oem<NN, NE>(v);
+#pragma unroll
+  for (int i = 0; i < NE; i++) if ((uint32_t)i < N) dst[i] = v[i];
 }
 
 template <class A>
@@ -878,11 +926,11 @@ constexpr int CCW = 128;    // pre-drawn candidates per round per warp
 
 struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
   uint32_t* sorted; uint32_t* a; float* vy; float* vz; uint8_t* cell; uint8_t* mod;
-  uint32_t* cij; uint32_t* cur; float* cp; float* cq; float* mg2; uint32_t* nacc;
+  uint32_t* cij; uint32_t* cur; float* cp; float* cq; float* ce; float* mg2; uint32_t* nacc;
 };
 
 __host__ __device__ inline size_t warp_smem_bytes(int capw) {
-  return (size_t)capw * 18 + (size_t)CCW * 16 + 32 * 8 + 16;
+  return (size_t)capw * 18 + (size_t)CCW * 20 + 32 * 8 + 16;
 }
 
 __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
@@ -895,7 +943,8 @@ __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
   w.cur = w.cij + CCW;
   w.cp = reinterpret_cast<float*>(w.cur + CCW);
   w.cq = w.cp + CCW;
-  w.mg2 = w.cq + CCW;
+  w.ce = w.cq + CCW;
+  w.mg2 = w.ce + CCW;
   w.nacc = reinterpret_cast<uint32_t*>(w.mg2 + 32);
   w.cell = reinterpret_cast<uint8_t*>(w.nacc + 32);
   w.mod = w.cell + capw;
@@ -969,18 +1018,26 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
         if (q < cnt) W.a[q] = v[u];
       }
     }
-    if (valid) for (uint32_t i = 0; i < N; i++) W.cell[off + i] = (uint8_t)lane;
+    // largest segment of the warp (network width); element -> cell tags only
+    // where the rank sort or the multi-run paths need them
+    const uint32_t wN = __reduce_max_sync(FULL, valid ? N : 0u);
+    if (valid && (wN > 32 || !one_run)) for (uint32_t i = 0; i < N; i++) W.cell[off + i] = (uint8_t)lane;
     __syncwarp();
-    // ---- C
-    if (valid && N <= (uint32_t)NET) {
-      uint32_t v[NET];
-#pragma unroll
-      for (int i = 0; i < NET; i++) v[i] = (uint32_t)i < N ? W.a[off + i] : 0xFFFFFFFFu;
-      sort_net<NET>(v);
-#pragma unroll
-      for (int i = 0; i < NET; i++) if ((uint32_t)i < N) W.sorted[off + i] = v[i];
-    }
-    if (__any_sync(FULL, valid && N > (uint32_t)NET)) {
+    // ---- C: network width by the warp's largest segment (warp-uniform)
+    if (wN <= 32) {
+      if (valid && N > 0) {
+        const uint32_t* src = W.a + off;
+        uint32_t* dst = W.sorted + off;
+        if (wN <= 4) sort_segment<4, 4>(src, dst, N);
+        else if (wN <= 8) sort_segment<8, 8>(src, dst, N);
+        else if (wN <= 12) sort_segment<16, 12>(src, dst, N);
+        else if (wN <= 16) sort_segment<16, 16>(src, dst, N);
+        else if (wN <= 20) sort_segment<32, 20>(src, dst, N);
+        else if (wN <= 24) sort_segment<32, 24>(src, dst, N);
+        else sort_segment<32, 32>(src, dst, N);
+      }
+    } else {
+      if (valid && N <= (uint32_t)NET) sort_segment<NET, NET>(W.a + off, W.sorted + off, N);
       for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
         const uint32_t q = q0 + lane;
         const int cq = q < cnt ? W.cell[q] : 0;
@@ -1115,6 +1172,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
         // two candidates per lane per pass: four independent Philox chains in flight
         for (uint32_t q0 = 0; q0 < lim; q0 += 64) {
           uint32_t qq[2], kq[2], nc[2], cc[2];
+          double gq_hat[2];
           int rc[2];
 #pragma unroll
           for (int hh = 0; hh < 2; hh++) {
@@ -1128,6 +1186,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
               if (m <= gq && lo + stp < 32) lo += stp;
             }
             nc[hh] = __shfl_sync(FULL, N, lo);
+            gq_hat[hh] = __shfl_sync(FULL, ghatu, lo);
             kq[hh] = gq - __shfl_sync(FULL, mst, lo);
             rc[hh] = __shfl_sync(FULL, r, lo);
             cc[hh] = __shfl_sync(FULL, c, lo);
@@ -1147,7 +1206,14 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
               uint32_t j = lemire(wp[hh].y, nc[hh] - 1);
               if (j >= i) j++;
               W.cij[q] = i | (j << 16);
-              W.cur[q] = wp[hh].z;
+              if (P.model == 0) {
+                // HS: accept iff (double)g2 > (u ghat)^2 (R13)  <=>  g2 > F, F the largest
+                // float <= (u ghat)^2 -- the same decision as one fp32 compare in the walk
+                const double lhs = u_co_d(wp[hh].z) * gq_hat[hh];
+                W.cur[q] = __float_as_uint(__double2float_rd(lhs * lhs));
+              } else {
+                W.cur[q] = wp[hh].z;
+              }
               // Marsaglia pair: first block drawn above, further blocks only if both tries fail
               float pp = 2.0f * u_co(wd[hh].x) - 1.0f, qv = 2.0f * u_co(wd[hh].y) - 1.0f;
               if (!(pp * pp + qv * qv < 1.0f)) {
@@ -1156,8 +1222,12 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
                 if (!(pp * pp + qv * qv < 1.0f))
                   marsaglia_pq_from(run_key(P, rc[hh]), cc[hh], (uint32_t)s, kq[hh], 1, pp, qv);
               }
-              W.cp[q] = pp;
-              W.cq[q] = qv;
+              // unit vector of R14, drawn ahead of use
+              const float rho = pp * pp + qv * qv;
+              const float sr = sqrtf(1.0f - rho);
+              W.cp[q] = 2.0f * pp * sr;
+              W.cq[q] = 2.0f * qv * sr;
+              W.ce[q] = 1.0f - 2.0f * rho;
             }
           }
         }
@@ -1166,8 +1236,8 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
           const uint32_t a0 = mstu > base ? mstu : base;
           const uint32_t a1 = mstu + Mu < base + lim ? mstu + Mu : base + lim;
           if (a0 < a1)
-            ntc_apply(P, Au, gmu, ghatu, W.cij + (a0 - base), W.cur + (a0 - base), W.cp + (a0 - base),
-                      W.cq + (a0 - base), a1 - a0, maxg2, naccu);
+            ntc_apply_pre(P, Au, gmu, W.cij + (a0 - base), W.cur + (a0 - base), W.cp + (a0 - base),
+                          W.cq + (a0 - base), W.ce + (a0 - base), a1 - a0, maxg2, naccu);
         }
         __syncwarp();
       }
@@ -1711,6 +1781,8 @@ static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t s
   static size_t configured = 0;
   if (smem > configured) {
     cudaFuncSetAttribute(k_collide<D, NET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (const char* e = getenv("DSMC_CARVEOUT"))   // A/B experiments: shared-memory carveout (percent)
+      cudaFuncSetAttribute(k_collide<D, NET>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
     configured = smem;
   }
   k_collide<D, NET><<<g, WPB * 32, smem, st>>>(P, mode, slot, capw);
