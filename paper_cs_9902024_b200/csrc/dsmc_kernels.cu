@@ -921,7 +921,7 @@ __device__ void heap_sort(uint32_t* a, uint32_t n) {
 //      candidates in increasing k -- the method's sequential order
 //   F  write modified velocities back (or the whole tile to its new rank)
 // mode 0: full step; mode 1: sample only into `slot_arg` (dsmc_sample).
-constexpr int WPB = 4;      // warps per block
+constexpr int WPB = 1;      // warps per block (1: the tile index, hence run and key, is uniform)
 constexpr int CCW = 128;    // pre-drawn candidates per round per warp
 
 struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
@@ -949,6 +949,77 @@ __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
   w.cell = reinterpret_cast<uint8_t*>(w.nacc + 32);
   w.mod = w.cell + capw;
   return w;
+}
+
+// E1 of k_collide: candidates [base, base + lim) of the tile drawn lane-parallel
+// (two per lane per pass: four independent Philox chains in flight); owner
+// cell of a candidate = last lane with prefix mst <= index.  UK: the tile
+// lies in one run, whose key key_u is then warp-uniform.
+template <bool UK>
+__device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int lane, uint32_t base, uint32_t lim,
+                                            uint32_t mst, uint32_t N, double ghatu, int r, uint32_t c, uint32_t s,
+                                            uint2 key_u) {
+    for (uint32_t q0 = 0; q0 < lim; q0 += 64) {
+      uint32_t qq[2], kq[2], nc[2], cc[2];
+      double gq_hat[2];
+      int rc[2];
+#pragma unroll
+      for (int hh = 0; hh < 2; hh++) {
+        qq[hh] = q0 + 32 * hh + lane;
+        const uint32_t gq = base + qq[hh];
+        // owning cell of candidate gq: last lane with mst <= gq (binary search over lanes)
+        int lo = 0;
+#pragma unroll
+        for (int stp = 16; stp > 0; stp >>= 1) {
+          const uint32_t m = __shfl_sync(FULL, mst, lo + stp);
+          if (m <= gq && lo + stp < 32) lo += stp;
+        }
+        nc[hh] = __shfl_sync(FULL, N, lo);
+        gq_hat[hh] = __shfl_sync(FULL, ghatu, lo);
+        kq[hh] = gq - __shfl_sync(FULL, mst, lo);
+        rc[hh] = __shfl_sync(FULL, r, lo);
+        cc[hh] = __shfl_sync(FULL, c, lo);
+      }
+      uint4 wp[2], wd[2];
+#pragma unroll
+      for (int hh = 0; hh < 2; hh++) {
+        const uint2 keyc = UK ? key_u : run_key(P, rc[hh]);
+        wp[hh] = draw(keyc, cc[hh], s, TAG_COLL_PAIR, kq[hh], 0);
+        wd[hh] = draw(keyc, cc[hh], s, TAG_COLL_DIR, kq[hh], 0);
+      }
+#pragma unroll
+      for (int hh = 0; hh < 2; hh++) {
+        const uint32_t q = qq[hh];
+        if (q < lim) {
+          const uint32_t i = lemire(wp[hh].x, nc[hh]);
+          uint32_t j = lemire(wp[hh].y, nc[hh] - 1);
+          if (j >= i) j++;
+          W.cij[q] = i | (j << 16);
+          if (P.model == 0) {
+            // HS: accept iff (double)g2 > (u ghat)^2 (R13)  <=>  g2 > F, F the largest
+            // float <= (u ghat)^2 -- the same decision as one fp32 compare in the walk
+            const double lhs = u_co_d(wp[hh].z) * gq_hat[hh];
+            W.cur[q] = __float_as_uint(__double2float_rd(lhs * lhs));
+          } else {
+            W.cur[q] = wp[hh].z;
+          }
+          // Marsaglia pair: first block drawn above, further blocks only if both tries fail
+          float pp = 2.0f * u_co(wd[hh].x) - 1.0f, qv = 2.0f * u_co(wd[hh].y) - 1.0f;
+          if (!(pp * pp + qv * qv < 1.0f)) {
+            pp = 2.0f * u_co(wd[hh].z) - 1.0f;
+            qv = 2.0f * u_co(wd[hh].w) - 1.0f;
+            if (!(pp * pp + qv * qv < 1.0f))
+              marsaglia_pq_from(UK ? key_u : run_key(P, rc[hh]), cc[hh], s, kq[hh], 1, pp, qv);
+          }
+          // unit vector of R14, drawn ahead of use
+          const float rho = pp * pp + qv * qv;
+          const float sr = sqrtf(1.0f - rho);
+          W.cp[q] = 2.0f * pp * sr;
+          W.cq[q] = 2.0f * qv * sr;
+          W.ce[q] = 1.0f - 2.0f * rho;
+        }
+      }
+    }
 }
 
 template <int D, int NET>
@@ -1103,16 +1174,37 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
           }
         }
       } else {
-        for (uint32_t q0 = 0; q0 < cnt; q0 += 256) {
+        // full 256-element rounds 8 deep without predicates, then the tail 2 deep
+        uint32_t q0 = 0;
+        for (; q0 + 256 <= cnt; q0 += 256) {
           uint32_t gg[8];
           float vv[8][3];
 #pragma unroll
+          for (int u = 0; u < 8; u++) gg[u] = W.sorted[q0 + 32 * u + lane];
+#pragma unroll
           for (int u = 0; u < 8; u++) {
+            vv[u][0] = sx[gg[u]];
+            vv[u][1] = sy[gg[u]];
+            vv[u][2] = sz[gg[u]];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            const uint32_t q = q0 + 32 * u + lane;
+            wvx[q] = vv[u][0];
+            W.vy[q] = vv[u][1];
+            W.vz[q] = vv[u][2];
+          }
+        }
+        for (; q0 < cnt; q0 += 64) {
+          uint32_t gg[2];
+          float vv[2][3];
+#pragma unroll
+          for (int u = 0; u < 2; u++) {
             const uint32_t q = q0 + 32 * u + lane;
             gg[u] = q < cnt ? W.sorted[q] : 0u;
           }
 #pragma unroll
-          for (int u = 0; u < 8; u++) {
+          for (int u = 0; u < 2; u++) {
             if (q0 + 32 * u + lane < cnt) {
               vv[u][0] = sx[gg[u]];
               vv[u][1] = sy[gg[u]];
@@ -1120,7 +1212,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
             }
           }
 #pragma unroll
-          for (int u = 0; u < 8; u++) {
+          for (int u = 0; u < 2; u++) {
             const uint32_t q = q0 + 32 * u + lane;
             if (q < cnt) {
               wvx[q] = vv[u][0];
@@ -1170,67 +1262,10 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
       for (uint32_t base = 0; base < tot; base += CCW) {
         const uint32_t lim = tot - base < (uint32_t)CCW ? tot - base : (uint32_t)CCW;
         // two candidates per lane per pass: four independent Philox chains in flight
-        for (uint32_t q0 = 0; q0 < lim; q0 += 64) {
-          uint32_t qq[2], kq[2], nc[2], cc[2];
-          double gq_hat[2];
-          int rc[2];
-#pragma unroll
-          for (int hh = 0; hh < 2; hh++) {
-            qq[hh] = q0 + 32 * hh + lane;
-            const uint32_t gq = base + qq[hh];
-            // owning cell of candidate gq: last lane with mst <= gq (binary search over lanes)
-            int lo = 0;
-#pragma unroll
-            for (int stp = 16; stp > 0; stp >>= 1) {
-              const uint32_t m = __shfl_sync(FULL, mst, lo + stp);
-              if (m <= gq && lo + stp < 32) lo += stp;
-            }
-            nc[hh] = __shfl_sync(FULL, N, lo);
-            gq_hat[hh] = __shfl_sync(FULL, ghatu, lo);
-            kq[hh] = gq - __shfl_sync(FULL, mst, lo);
-            rc[hh] = __shfl_sync(FULL, r, lo);
-            cc[hh] = __shfl_sync(FULL, c, lo);
-          }
-          uint4 wp[2], wd[2];
-#pragma unroll
-          for (int hh = 0; hh < 2; hh++) {
-            const uint2 keyc = run_key(P, rc[hh]);
-            wp[hh] = draw(keyc, cc[hh], (uint32_t)s, TAG_COLL_PAIR, kq[hh], 0);
-            wd[hh] = draw(keyc, cc[hh], (uint32_t)s, TAG_COLL_DIR, kq[hh], 0);
-          }
-#pragma unroll
-          for (int hh = 0; hh < 2; hh++) {
-            const uint32_t q = qq[hh];
-            if (q < lim) {
-              const uint32_t i = lemire(wp[hh].x, nc[hh]);
-              uint32_t j = lemire(wp[hh].y, nc[hh] - 1);
-              if (j >= i) j++;
-              W.cij[q] = i | (j << 16);
-              if (P.model == 0) {
-                // HS: accept iff (double)g2 > (u ghat)^2 (R13)  <=>  g2 > F, F the largest
-                // float <= (u ghat)^2 -- the same decision as one fp32 compare in the walk
-                const double lhs = u_co_d(wp[hh].z) * gq_hat[hh];
-                W.cur[q] = __float_as_uint(__double2float_rd(lhs * lhs));
-              } else {
-                W.cur[q] = wp[hh].z;
-              }
-              // Marsaglia pair: first block drawn above, further blocks only if both tries fail
-              float pp = 2.0f * u_co(wd[hh].x) - 1.0f, qv = 2.0f * u_co(wd[hh].y) - 1.0f;
-              if (!(pp * pp + qv * qv < 1.0f)) {
-                pp = 2.0f * u_co(wd[hh].z) - 1.0f;
-                qv = 2.0f * u_co(wd[hh].w) - 1.0f;
-                if (!(pp * pp + qv * qv < 1.0f))
-                  marsaglia_pq_from(run_key(P, rc[hh]), cc[hh], (uint32_t)s, kq[hh], 1, pp, qv);
-              }
-              // unit vector of R14, drawn ahead of use
-              const float rho = pp * pp + qv * qv;
-              const float sr = sqrtf(1.0f - rho);
-              W.cp[q] = 2.0f * pp * sr;
-              W.cq[q] = 2.0f * qv * sr;
-              W.ce[q] = 1.0f - 2.0f * rho;
-            }
-          }
-        }
+        if (one_run)
+          ntc_predraw<true>(P, W, lane, base, lim, mst, N, ghatu, r, c, (uint32_t)s, run_key(P, r_first));
+        else
+          ntc_predraw<false>(P, W, lane, base, lim, mst, N, ghatu, r, c, (uint32_t)s, run_key(P, r_first));
         __syncwarp();
         if (Mu) {
           const uint32_t a0 = mstu > base ? mstu : base;
@@ -1264,12 +1299,21 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
         float* __restrict__ vxp = (h ? P1 : P0) + 3 * RS;
         float* __restrict__ vyp = vxp + RS;
         float* __restrict__ vzp = vyp + RS;
-        for (uint32_t q = lane; q < cnt; q += 32) {
-          if (W.mod[q]) {
-            const uint32_t g = W.sorted[q];
-            vxp[g] = wvx[q];
-            vyp[g] = W.vy[q];
-            vzp[g] = W.vz[q];
+        // collided flags read four at a time
+        const uint32_t* m32 = reinterpret_cast<const uint32_t*>(W.mod);
+        for (uint32_t w = lane; w < (cnt + 3) / 4; w += 32) {
+          const uint32_t m = m32[w];
+          if (m) {
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+              if (m & (0xFFu << (8 * b))) {
+                const uint32_t q = 4 * w + b;
+                const uint32_t g = W.sorted[q];
+                vxp[g] = wvx[q];
+                vyp[g] = W.vy[q];
+                vzp[g] = W.vz[q];
+              }
+            }
           }
         }
       }
