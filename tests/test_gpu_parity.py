@@ -307,3 +307,68 @@ def test_full_size_sampled_parity(dsmc_gpu, oracle_mod, name, warm, run):
     assert np.array_equal(sim.get_gmax(run), ref.get_gmax())
     if name == "c5":
         assert int(gi["count"].max()) > 256      # dense cells exist: heavy tiles were exercised
+
+
+@pytest.mark.parametrize("name", ["c1", "c2_small", "c3_small", "c4_small", "c5_small"])
+def test_multi_step_call_matches_oracle(dsmc_gpu, oracle_mod, name):
+    """From the fill, 9 steps in one dsmc_step call (graph replays, reorder and
+    sample steps included) reproduce the oracle's trajectory of every run checked."""
+    p = configs.get(name)
+    sim = dsmc_gpu.Simulation(p, debug=True)
+    sim.generate()
+    sim.step(9)
+    rc, cnt = sim.status()
+    assert rc == 0
+    for run in sorted({0, p["n_runs"] - 1}):
+        ref = oracle_mod.OracleRun(p, run)
+        ref.fill()
+        ref.step(9)
+        compare_state(sim.get_state(run), ref.get_state(), p, tag=f"{name} run {run}")
+        gi, oi = sim.get_index(run), ref.get_index()
+        assert np.array_equal(gi["lcr"], oi["lcr"])
+        cand, acc = ref.get_cell_stats()
+        assert np.array_equal(gi["cand"], cand) and np.array_equal(gi["acc"], acc)
+        oc = ref.counters()
+        for key in ("inserted", "removed", "candidates", "accepted"):
+            assert cnt[run][key] == oc[key], (name, run, key)
+
+
+@pytest.mark.parametrize("name", ["c2_small", "c3_small", "c4_small", "c5_small", "heavy"])
+def test_one_call_equals_single_steps(dsmc_gpu, name):
+    """One 12-step call and twelve 1-step calls give bit-identical state,
+    counters and snapshots (also with heavy and giant cells)."""
+    def make():
+        if name != "heavy":
+            p = configs.get(name)
+            sim = dsmc_gpu.Simulation(p)
+            sim.generate()
+            return p, sim
+        p = configs.get("c4_small")
+        p["reorder_every"] = 3
+        p["fill"] = []
+        st = inputs.clustered_state(4, p, [5, 6, 7, 300, 301, 2000], 700)
+        st2 = inputs.clustered_state(5, p, [9], 9000)
+        for k in st:
+            st[k] = np.concatenate([st[k], st2[k]])
+        p["cap_per_run"] = len(st["x"]) + 64
+        sim = dsmc_gpu.Simulation(p)
+        sim.generate()
+        for r in range(p["n_runs"]):
+            sim.set_state(r, st, step=0)
+        return p, sim
+    p, a = make()
+    _, b = make()
+    a.step(12)
+    for _ in range(12):
+        b.step(1)
+    ra, ca = a.status()
+    rb, cb = b.status()
+    assert ra == 0 and rb == 0
+    assert ca == cb
+    for r in range(p["n_runs"]):
+        sa, sb = a.get_state(r), b.get_state(r)
+        for k in sa:
+            assert np.array_equal(sa[k], sb[k]), (name, r, k)
+        assert np.array_equal(a.get_gmax(r), b.get_gmax(r))
+    for slot in range(min(configs.n_slots(p), 12 // configs.sample_every(p))):
+        assert np.array_equal(a.read_sums(slot), b.read_sums(slot))

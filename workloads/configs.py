@@ -96,7 +96,9 @@ def c4(n_runs=256, n_steps=100, sample_every=10):
         dim=3, nx=64, ny=64, nz=64, fnum_vc=N_D_LAMBDA1 / 10.0, model=HS,
         bc=[PERIODIC] * 6,
         fill=[dict(lo=[0, 0, 0], hi=[64, 64, 64], ppc=10, T=1.0, u=[0.0, 0.0, 0.0])],
-        seed=4, n_runs=n_runs, reorder_every=4, cap_per_run=64 * 64 * 64 * 10,
+        # physical reorder every 2 steps (measured on B200 at n = 256: 21.8 ms/step
+        # against 22.4 for K = 4 and 22.0 for K = 3; K is a problem parameter)
+        seed=4, n_runs=n_runs, reorder_every=2, cap_per_run=64 * 64 * 64 * 10,
         **_clock(0.2, n_steps, sample_every))
 
 
