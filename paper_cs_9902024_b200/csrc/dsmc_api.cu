@@ -335,6 +335,10 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   P.ctl.queue = (unsigned long long*)(ct + L.c_queue);
   P.ctl.heavy = (uint32_t*)(ct + L.c_heavy);
   P.heavy_list = (uint32_t*)(sc + L.s_heavy);
+  // NEXT-1 A/B: DSMC_STATIC_CELLS=1 disables the heavy-tile queue, so
+  // overflowing tiles stay with their warp (lane = cell, global memory): the
+  // static mapping against which the TLPDPR-style reallocation is measured
+  if (const char* e = std::getenv("DSMC_STATIC_CELLS")) if (std::atoi(e)) P.heavy_list = nullptr;
   P.caph = 8192;
 
   auto bail = [&](int code) { delete c; return code; };

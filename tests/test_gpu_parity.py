@@ -372,3 +372,34 @@ def test_one_call_equals_single_steps(dsmc_gpu, name):
         assert np.array_equal(a.get_gmax(r), b.get_gmax(r))
     for slot in range(min(configs.n_slots(p), 12 // configs.sample_every(p))):
         assert np.array_equal(a.read_sums(slot), b.read_sums(slot))
+
+
+def test_static_cell_mapping_equals_heavy_queue(dsmc_gpu, monkeypatch):
+    """NEXT-1 A/B switch: with the heavy-tile queue disabled (static lane = cell
+    mapping in global memory) the results are bit-identical."""
+    def run(static):
+        if static:
+            monkeypatch.setenv("DSMC_STATIC_CELLS", "1")
+        else:
+            monkeypatch.delenv("DSMC_STATIC_CELLS", raising=False)
+        p = configs.get("c4_small")
+        p["reorder_every"] = 3
+        p["fill"] = []
+        st = inputs.clustered_state(4, p, [5, 6, 7, 300, 301, 2000], 700)
+        st2 = inputs.clustered_state(5, p, [9], 3000)
+        for k in st:
+            st[k] = np.concatenate([st[k], st2[k]])
+        p["cap_per_run"] = len(st["x"]) + 64
+        sim = dsmc_gpu.Simulation(p)
+        sim.generate()
+        for r in range(p["n_runs"]):
+            sim.set_state(r, st, step=0)
+        sim.step(5)
+        return sim, p
+    a, p = run(False)
+    b, _ = run(True)
+    assert a.status()[1] == b.status()[1]
+    for r in range(p["n_runs"]):
+        sa, sb = a.get_state(r), b.get_state(r)
+        for k in sa:
+            assert np.array_equal(sa[k], sb[k]), k
