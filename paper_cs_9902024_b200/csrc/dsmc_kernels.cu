@@ -654,6 +654,21 @@ struct GlobCell {
   __device__ void st(uint32_t i, const float a[3]) const { const uint32_t g = idx[i]; vx[g] = a[0]; vy[g] = a[1]; vz[g] = a[2]; }
 };
 
+// VHS acceptance of R13, u (sigma g)_max < sigma_c (g^2)^(1-omega), decided
+// exactly but mostly without the fp64 pow: the two sides are first compared
+// as fp32 base-2 logarithms (MUFU.LG2, absolute error < 2^-21 over the range
+// used, plus the float roundings of both arguments, all far below 2^-10), and
+// only a decision within 2^-10 of the threshold -- about one candidate in a
+// thousand -- evaluates the fp64 expression itself.
+__device__ __forceinline__ bool vhs_accept(const Prm& P, uint32_t uword, double gm, float g2) {
+  const double lhs = u_co_d(uword) * gm;
+  const float l_lhs = __log2f((float)lhs);
+  const float l_rhs = __log2f((float)P.sigma_c) + (float)P.omega1 * __log2f(g2);
+  if (l_lhs < l_rhs - 0.0009765625f) return true;      // lhs < rhs by more than a factor 2^(1/1024)
+  if (l_lhs > l_rhs + 0.0009765625f) return false;
+  return lhs < P.sigma_c * pow((double)g2, P.omega1);   // near the threshold (and 0, inf cases): exact
+}
+
 // NTC in one cell (readings R12-R15): M = floor(1/2 N(N-1) coef gmax + u);
 // candidate k: i = lemire(a, N), j = lemire(b, N-1) (+1 if >= i); accept iff
 // u (sigma g)_max < sigma g in fp64; g_max frozen during the step.
@@ -686,7 +701,7 @@ __device__ __forceinline__ void collide_cell(const Prm& P, uint2 key, uint32_t c
       const double lhs = u_co_d(w.z) * ghat;
       accept = lhs * lhs < (double)g2;
     } else {
-      accept = u_co_d(w.z) * gm < P.sigma_c * pow((double)g2, P.omega1);
+      accept = vhs_accept(P, w.z, gm, g2);
     }
     if (accept) {
       float e[3];
@@ -776,7 +791,7 @@ __device__ __forceinline__ void ntc_apply(const Prm& P, const A& acc, double gm,
       const double lhs = u_co_d(ur[k]) * ghat;
       accept = lhs * lhs < (double)g2;
     } else {
-      accept = u_co_d(ur[k]) * gm < P.sigma_c * pow((double)g2, P.omega1);
+      accept = vhs_accept(P, ur[k], gm, g2);
     }
     if (accept) {
       const float pp = cp[k], qq = cq[k];
@@ -811,7 +826,7 @@ __device__ __forceinline__ void ntc_apply_pre(const Prm& P, const A& acc, double
     const float g2 = (dx * dx + dy * dy) + dz * dz;
     maxg2 = g2 > maxg2 ? g2 : maxg2;
     const bool accept = P.model == 0 ? g2 > __uint_as_float(thr[k])
-                                     : u_co_d(thr[k]) * gm < P.sigma_c * pow((double)g2, P.omega1);
+                                     : vhs_accept(P, thr[k], gm, g2);
     if (accept) {
       const float e[3] = {ex[k], ey[k], ez[k]};
       const float cmx = (a[0] + b[0]) * 0.5f, cmy = (a[1] + b[1]) * 0.5f, cmz = (a[2] + b[2]) * 0.5f;

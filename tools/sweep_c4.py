@@ -17,7 +17,7 @@ for n in (1, 4, 16, 64, 256):
         continue
     d = json.loads(line[-1])
     rows.append((n, d, None))
-lines = [f"# {tag}: c4 batching sweep (64^3 cells x 10 ppc per run, HS, K=4, 20 timed steps)\n",
+lines = [f"# {tag}: c4 batching sweep (64^3 cells x 10 ppc per run, HS, K=2, 20 timed steps)\n",
          "| n runs | particles | ms/step | particle-steps/s | collide share | collide GB/s (alg.) |", "|---|---|---|---|---|---|"]
 for n, d, err in rows:
     if d is None:
