@@ -128,6 +128,20 @@ int dsmc_step(dsmc_ctx* ctx, int32_t nsteps);
 /* Explicit Sampling of the current state into slot (re-enumerates; no collisions). */
 int dsmc_sample(dsmc_ctx* ctx, int32_t slot);
 
+/* Time averaging for steady problems ("we have to increase the
+ * time interval of averaging ... after steady state is achieved", Delta t_av >>
+ * Delta t): ADDS the current state's per-cell sums (N, sum v, sum |v|^2, fp64)
+ * to slot `slot` of array C and counts one more sample in it; a slot never
+ * written before starts from zero.  dsmc_read_macros then divides the density by
+ * n_runs * m (m = samples in the slot); velocity and temperature are pooled
+ * ratios of the accumulated sums (reading R18).  A scheduled Sampling of the
+ * unsteady clock, or dsmc_sample, overwrites the slot (m = 1).  Asynchronous;
+ * DSMC_ESCHED for a slot out of range. */
+int dsmc_sample_add(dsmc_ctx* ctx, int32_t slot);
+
+/* SYNC. Samples accumulated in slot (0: never written; 1: a snapshot). */
+int dsmc_slot_samples(dsmc_ctx* ctx, int32_t slot, int32_t* out);
+
 /* SYNC. Ensemble analysis of one slot: per cell, pooled
  * over runs in ascending run id, rho, ux, uy, uz, T then their leave-one-run-
  * out jackknife standard errors -> host out[Nc][10] (fp64). */

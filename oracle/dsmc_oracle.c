@@ -56,7 +56,7 @@ struct orc_run {
   int32_t* acc;
   float* gmax;
   double* snap;
-  uint8_t* snap_done;
+  int32_t* snap_done;        /* samples accumulated in the slot (0 = never written) */
   int64_t inserted, removed, candidates, accepted;
 };
 
@@ -225,7 +225,7 @@ orc_run* orc_create(const orc_problem* p, int32_t run_id, int32_t* err) {
   R->cand = (int64_t*)calloc((size_t)R->Nc, sizeof(int64_t));
   R->acc = (int32_t*)calloc((size_t)R->Nc, sizeof(int32_t));
   R->snap = (double*)calloc((size_t)R->n_slots * 5 * (size_t)R->Nc, sizeof(double));
-  R->snap_done = (uint8_t*)calloc((size_t)R->n_slots, 1);
+  R->snap_done = (int32_t*)calloc((size_t)R->n_slots, sizeof(int32_t));
   return R;
 }
 
@@ -586,8 +586,10 @@ static void interaction(orc_run* R, int32_t s) {
 
 /* ------------------------------------------------------------ Sampling -- */
 /* Sampling (array C, 121-123): per cell N, sum v,
- * sum |v|^2 in fp64, summed sequentially in LCR (canonical) order. */
-static void sampling(orc_run* R, int32_t slot) {
+ * sum |v|^2 in fp64, summed sequentially in LCR (canonical) order.  add = 1:
+ * the sums are added to the slot's -- time averaging over Delta t_av >> Delta t
+ * for steady problems -- and its sample count grows by one. */
+static void sampling(orc_run* R, int32_t slot, int add) {
   double* S = R->snap + (size_t)slot * 5 * (size_t)R->Nc;
   for (int64_t c = 0; c < R->Nc; c++) {
     double sn = 0, sx = 0, sy = 0, sz = 0, se = 0;
@@ -597,18 +599,37 @@ static void sampling(orc_run* R, int32_t slot) {
       sn += 1.0; sx += vx; sy += vy; sz += vz;
       se += (vx * vx + vy * vy) + vz * vz;
     }
-    S[0 * R->Nc + c] = sn; S[1 * R->Nc + c] = sx; S[2 * R->Nc + c] = sy;
-    S[3 * R->Nc + c] = sz; S[4 * R->Nc + c] = se;
+    if (add) {
+      S[0 * R->Nc + c] += sn; S[1 * R->Nc + c] += sx; S[2 * R->Nc + c] += sy;
+      S[3 * R->Nc + c] += sz; S[4 * R->Nc + c] += se;
+    } else {
+      S[0 * R->Nc + c] = sn; S[1 * R->Nc + c] = sx; S[2 * R->Nc + c] = sy;
+      S[3 * R->Nc + c] = sz; S[4 * R->Nc + c] = se;
+    }
   }
-  R->snap_done[slot] = 1;
+  R->snap_done[slot] = add ? R->snap_done[slot] + 1 : 1;
 }
 
 int32_t orc_sample(orc_run* R, int32_t slot) {
   if (slot < 0 || slot >= R->n_slots) return ORC_ESCHED;
   enumeration(R);
   indexing(R);
-  sampling(R, slot);
+  sampling(R, slot, 0);
   return R->status;
+}
+
+int32_t orc_sample_add(orc_run* R, int32_t slot) {
+  if (slot < 0 || slot >= R->n_slots) return ORC_ESCHED;
+  if (!R->snap_done[slot]) memset(R->snap + (size_t)slot * 5 * (size_t)R->Nc, 0, sizeof(double) * 5 * (size_t)R->Nc);
+  enumeration(R);
+  indexing(R);
+  sampling(R, slot, 1);
+  return R->status;
+}
+
+int32_t orc_snap_count(const orc_run* R, int32_t slot) {
+  if (slot < 0 || slot >= R->n_slots) return -1;
+  return R->snap_done[slot];
 }
 
 /* ------------------------------------------------------------- Reorder -- */
@@ -640,7 +661,7 @@ int32_t orc_step(orc_run* R) {
   interaction(R, s);
   if ((s + 1) % R->sample_every == 0) {
     int32_t slot = (s + 1) / R->sample_every - 1;
-    if (slot < R->n_slots) sampling(R, slot);
+    if (slot < R->n_slots) sampling(R, slot, 0);
   }
   int K = R->p.reorder_every;
   if ((K > 0 && (s + 1) % K == 0) || R->cap - R->n < R->insert_bound) reorder(R);
@@ -722,13 +743,17 @@ static void moments(double sn, double sx, double sy, double sz, double se, doubl
   }
 }
 
-void orc_ensemble(int32_t n_runs, int64_t Nc, const double* sums, double fnum_vc, double* out) {
+/* Ensemble of one slot over runs (reading R18), each run's
+ * sums holding m samples (m = 1: a snapshot; m > 1: time averaged):
+ * density = S_N F_N/V_c / (n m). */
+void orc_ensemble_m(int32_t n_runs, int64_t Nc, const double* sums, double fnum_vc, int32_t m, double* out) {
+  const double mm = m > 0 ? (double)m : 1.0;
   for (int64_t c = 0; c < Nc; c++) {
     double tot[5] = {0, 0, 0, 0, 0};
     for (int32_t r = 0; r < n_runs; r++)
       for (int q = 0; q < 5; q++) tot[q] += sums[((size_t)r * 5 + q) * (size_t)Nc + c];
     double full[5];
-    moments(tot[0], tot[1], tot[2], tot[3], tot[4], fnum_vc, (double)n_runs, full);
+    moments(tot[0], tot[1], tot[2], tot[3], tot[4], fnum_vc, (double)n_runs * mm, full);
     double* o = out + (size_t)c * 10;
     for (int q = 0; q < 5; q++) o[q] = full[q];
     if (n_runs < 2) { for (int q = 0; q < 5; q++) o[5 + q] = 0.0; continue; }
@@ -737,7 +762,7 @@ void orc_ensemble(int32_t n_runs, int64_t Nc, const double* sums, double fnum_vc
     for (int32_t r = 0; r < n_runs; r++) {
       double part[5];
       for (int q = 0; q < 5; q++) part[q] = tot[q] - sums[((size_t)r * 5 + q) * (size_t)Nc + c];
-      moments(part[0], part[1], part[2], part[3], part[4], fnum_vc, (double)(n_runs - 1), loo);
+      moments(part[0], part[1], part[2], part[3], part[4], fnum_vc, (double)(n_runs - 1) * mm, loo);
       for (int q = 0; q < 5; q++) { th[r * 5 + q] = loo[q]; mean[q] += loo[q]; }
     }
     for (int q = 0; q < 5; q++) mean[q] /= (double)n_runs;
@@ -748,4 +773,8 @@ void orc_ensemble(int32_t n_runs, int64_t Nc, const double* sums, double fnum_vc
     }
     free(th);
   }
+}
+
+void orc_ensemble(int32_t n_runs, int64_t Nc, const double* sums, double fnum_vc, double* out) {
+  orc_ensemble_m(n_runs, Nc, sums, fnum_vc, 1, out);
 }

@@ -62,6 +62,8 @@ int32_t  orc_fill_initial(orc_run* r);             /* Generation, initial fill *
 int32_t  orc_step(orc_run* r);                     /* one Fig. 1 inner-loop step */
 int32_t  orc_steps(orc_run* r, int32_t k);
 int32_t  orc_sample(orc_run* r, int32_t slot);     /* explicit Sampling of current state */
+int32_t  orc_sample_add(orc_run* r, int32_t slot); /* add current state's sums to the slot (time averaging) */
+int32_t  orc_snap_count(const orc_run* r, int32_t slot); /* samples in the slot (0: never written) */
 
 int64_t  orc_n_store(const orc_run* r);
 int32_t  orc_step_index(const orc_run* r);
@@ -94,6 +96,8 @@ int32_t  orc_n_face(const orc_run* r);
 
 /* Ensemble over runs ("one processor analyzes the results"):
  * sums [n_runs][5][Nc] -> out [Nc][10] = rho,ux,uy,uz,T, then jackknife SEs. */
+void     orc_ensemble_m(int32_t n_runs, int64_t Nc, const double* sums, double fnum_vc, int32_t m,
+                        double* out /* [Nc][10] */);
 void     orc_ensemble(int32_t n_runs, int64_t Nc, const double* sums, double fnum_vc,
                       double* out);
 

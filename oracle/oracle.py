@@ -93,6 +93,10 @@ def lib():
         L.orc_steps.argtypes = [vp, C.c_int32]
         L.orc_sample.restype = C.c_int32
         L.orc_sample.argtypes = [vp, C.c_int32]
+        L.orc_sample_add.restype = C.c_int32
+        L.orc_sample_add.argtypes = [vp, C.c_int32]
+        L.orc_snap_count.restype = C.c_int32
+        L.orc_snap_count.argtypes = [vp, C.c_int32]
         L.orc_n_store.restype = C.c_int64
         L.orc_n_store.argtypes = [vp]
         L.orc_counters.argtypes = [vp, vp]
@@ -114,6 +118,7 @@ def lib():
         L.orc_inflow_count.restype = C.c_int64
         L.orc_inflow_count.argtypes = [vp, C.c_int32, C.c_int32]
         L.orc_ensemble.argtypes = [C.c_int32, C.c_int64, vp, C.c_double, vp]
+        L.orc_ensemble_m.argtypes = [C.c_int32, C.c_int64, vp, C.c_double, C.c_int32, vp]
         L.orc_philox4x32_10.argtypes = [vp, vp, vp]
         _lib = L
     return _lib
@@ -131,12 +136,12 @@ def philox(ctr, key):
     return out
 
 
-def ensemble(sums, fnum_vc):
-    """sums: float64 [n_runs][5][Nc] -> [Nc][10]."""
+def ensemble(sums, fnum_vc, m=1):
+    """sums: float64 [n_runs][5][Nc], each run's holding m samples -> [Nc][10]."""
     sums = np.ascontiguousarray(sums, np.float64)
     n_runs, five, Nc = sums.shape
     out = np.zeros((Nc, 10), np.float64)
-    lib().orc_ensemble(n_runs, Nc, _ptr(sums), fnum_vc, _ptr(out))
+    lib().orc_ensemble_m(n_runs, Nc, _ptr(sums), fnum_vc, int(m), _ptr(out))
     return out
 
 
@@ -167,6 +172,13 @@ class OracleRun:
 
     def sample(self, slot):
         return lib().orc_sample(self.h, slot)
+
+    def sample_add(self, slot):
+        """Time averaging (steady problems): add the current state's sums to the slot."""
+        return lib().orc_sample_add(self.h, slot)
+
+    def snap_count(self, slot):
+        return lib().orc_snap_count(self.h, slot)
 
     @property
     def n(self):

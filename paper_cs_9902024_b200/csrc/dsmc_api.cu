@@ -452,11 +452,33 @@ int dsmc_kernels_per_step(dsmc_ctx* c, int32_t* out) {
   return DSMC_OK;
 }
 
+static int slot_written(dsmc_ctx* c, int32_t slot, bool* ok);
+
 int dsmc_sample(dsmc_ctx* c, int32_t slot) {
   if (!c) return fail(DSMC_EINVAL, "null ctx");
   if (slot < 0 || slot >= c->L.sz.n_slots) return fail(DSMC_ESCHED, "slot out of range");
-  dsmc::issue_sample(c->P, slot, c->stream);
+  dsmc::issue_sample(c->P, slot, 0, c->stream);
   CK(cudaGetLastError());
+  return DSMC_OK;
+}
+
+int dsmc_sample_add(dsmc_ctx* c, int32_t slot) {
+  if (!c) return fail(DSMC_EINVAL, "null ctx");
+  if (slot < 0 || slot >= c->L.sz.n_slots) return fail(DSMC_ESCHED, "slot out of range");
+  bool written = false;
+  const int rc = slot_written(c, slot, &written);
+  if (rc) return rc;
+  if (!written) CK(cudaMemsetAsync(c->P.C + (size_t)slot * 5 * (size_t)c->L.RN, 0, 8 * 5 * (size_t)c->L.RN, c->stream));
+  dsmc::issue_sample(c->P, slot, 1, c->stream);
+  CK(cudaGetLastError());
+  return DSMC_OK;
+}
+
+int dsmc_slot_samples(dsmc_ctx* c, int32_t slot, int32_t* out) {
+  if (!c || !out) return fail(DSMC_EINVAL, "bad argument");
+  if (slot < 0 || slot >= c->L.sz.n_slots) return fail(DSMC_ESCHED, "slot out of range");
+  CK(cudaMemcpyAsync(out, c->P.ctl.slot_done + slot, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
   return DSMC_OK;
 }
 

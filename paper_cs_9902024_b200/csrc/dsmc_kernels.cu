@@ -554,8 +554,8 @@ __device__ __forceinline__ uint32_t run_lcr_base(const Prm& P, int r) {
 __global__ void k_step_end(Prm P, int mode, int slot) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r == 0) { P.ctl.heavy[0] = 0; P.ctl.heavy[1] = 0; }   // heavy-tile queue of k_collide
-  if (mode == 1) {  // explicit sample
-    if (r == 0) P.ctl.slot_done[slot] = 1;
+  if (mode != 0) {  // explicit sample (1: snapshot, 2: added to the slot's time average)
+    if (r == 0) P.ctl.slot_done[slot] = mode == 1 ? 1 : P.ctl.slot_done[slot] + 1;
     return;
   }
   const int32_t s = *P.ctl.step;
@@ -877,8 +877,11 @@ __device__ __forceinline__ void sort_segment(const uint32_t* src, uint32_t* dst,
   for (int i = 0; i < NE; i++) if ((uint32_t)i < N) dst[i] = v[i];
 }
 
+// Sampling of one cell into slot `slot` of array C (R17); add: accumulate
+// (time averaging for steady problems) instead of overwrite
 template <class A>
-__device__ __forceinline__ void sample_cell(const Prm& P, int slot, int64_t k, uint32_t N, const A& acc) {
+__device__ __forceinline__ void sample_cell(const Prm& P, int slot, int64_t k, uint32_t N, const A& acc,
+                                            bool add = false) {
   double sx = 0.0, sy = 0.0, sz = 0.0, se = 0.0;
   for (uint32_t i = 0; i < N; i++) {
     float a[3];
@@ -889,7 +892,11 @@ __device__ __forceinline__ void sample_cell(const Prm& P, int slot, int64_t k, u
   }
   const int64_t RN = (int64_t)P.R * P.Nc;
   double* C = P.C + (int64_t)slot * 5 * RN + k;
-  C[0] = (double)N; C[RN] = sx; C[2 * RN] = sy; C[3 * RN] = sz; C[4 * RN] = se;
+  if (add) {
+    C[0] += (double)N; C[RN] += sx; C[2 * RN] += sy; C[3 * RN] += sz; C[4 * RN] += se;
+  } else {
+    C[0] = (double)N; C[RN] = sx; C[2 * RN] = sy; C[3 * RN] = sz; C[4 * RN] = se;
+  }
 }
 
 __device__ __forceinline__ void insertion_sort(uint32_t* a, uint32_t n) {
@@ -935,7 +942,8 @@ __device__ void heap_sort(uint32_t* a, uint32_t n) {
 //      acceptance word, Marsaglia pair), then each lane walks one cell's
 //      candidates in increasing k -- the method's sequential order
 //   F  write modified velocities back (or the whole tile to its new rank)
-// mode 0: full step; mode 1: sample only into `slot_arg` (dsmc_sample).
+// mode 0: full step; mode 1: sample only into `slot_arg` (dsmc_sample);
+// mode 2: sample added to `slot_arg` (dsmc_sample_add, time averaging).
 constexpr int WPB = 1;      // warps per block (1: the tile index, hence run and key, is uniform)
 constexpr int CCW = 128;    // pre-drawn candidates per round per warp
 
@@ -1297,7 +1305,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
         if (sgm > (double)gm) gm = (float)sgm;
       }
     }
-    if (valid && slot >= 0) sample_cell(P, slot, k, N, SmemCell{wvx + off, W.vy + off, W.vz + off, W.mod + off});
+    if (valid && slot >= 0) sample_cell(P, slot, k, N, SmemCell{wvx + off, W.vy + off, W.vz + off, W.mod + off}, mode == 2);
     __syncwarp();
     // ---- F
     if (one_run) {
@@ -1364,7 +1372,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
     else heap_sort(seg, N);
     GlobCell A{seg, parr(P, h, 3), parr(P, h, 4), parr(P, h, 5)};
     if (mode == 0) collide_cell(P, key, c, (uint32_t)s, N, A, gm, ncand, nacc);
-    if (slot >= 0) sample_cell(P, slot, k, N, A);
+    if (slot >= 0) sample_cell(P, slot, k, N, A, mode == 2);
     if (reo) {
       for (uint32_t i = 0; i < N; i++) {
         const uint32_t g = seg[i];
@@ -1615,7 +1623,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
       }
       if (valid && slot >= 0) {
         const uint32_t off = c_st[t] - S;
-        sample_cell(P, slot, k0 + t, N, SmemCell{s_vx + off, s_vy + off, s_vz + off, s_mod + off});
+        sample_cell(P, slot, k0 + t, N, SmemCell{s_vx + off, s_vy + off, s_vz + off, s_mod + off}, mode == 2);
       }
       __syncthreads();
       // ---- F: write back
@@ -1643,7 +1651,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
       else heap_sort(seg, N);
       GlobCell A{seg, parr(P, h, 3), parr(P, h, 4), parr(P, h, 5)};
       if (mode == 0) collide_cell(P, run_key(P, r), c, (uint32_t)s, N, A, gm, ncand, nacc);
-      if (slot >= 0) sample_cell(P, slot, k0 + t, N, A);
+      if (slot >= 0) sample_cell(P, slot, k0 + t, N, A, mode == 2);
       if (reo) {
         const uint32_t rb = c_base[t];
         for (uint32_t i = 0; i < N; i++) {
@@ -1690,8 +1698,11 @@ __global__ void k_macros(Prm P, int slot, double fnum_vc) {
   double tot[5] = {0, 0, 0, 0, 0};
   for (int r = 0; r < P.R; r++)
     for (int q = 0; q < 5; q++) tot[q] += C[q * RN + (int64_t)r * P.Nc + c];
+  // samples per run in the slot: 1 for a snapshot, m for a time average
+  const int32_t m_i = P.ctl.slot_done[slot];
+  const double m = m_i > 0 ? (double)m_i : 1.0;
   double full[5];
-  moments(tot[0], tot[1], tot[2], tot[3], tot[4], fnum_vc, (double)P.R, full);
+  moments(tot[0], tot[1], tot[2], tot[3], tot[4], fnum_vc, (double)P.R * m, full);
   double* o = P.macros + c * 10;
   for (int q = 0; q < 5; q++) o[q] = full[q];
   if (P.R < 2) { for (int q = 0; q < 5; q++) o[5 + q] = 0.0; return; }
@@ -1700,7 +1711,7 @@ __global__ void k_macros(Prm P, int slot, double fnum_vc) {
   for (int r = 0; r < P.R; r++) {
     double part[5], loo[5];
     for (int q = 0; q < 5; q++) part[q] = tot[q] - C[q * RN + (int64_t)r * P.Nc + c];
-    moments(part[0], part[1], part[2], part[3], part[4], fnum_vc, (double)(P.R - 1), loo);
+    moments(part[0], part[1], part[2], part[3], part[4], fnum_vc, (double)(P.R - 1) * m, loo);
     for (int q = 0; q < 5; q++) mean[q] += loo[q];
   }
   for (int q = 0; q < 5; q++) mean[q] /= (double)P.R;
@@ -1708,7 +1719,7 @@ __global__ void k_macros(Prm P, int slot, double fnum_vc) {
   for (int r = 0; r < P.R; r++) {
     double part[5], loo[5];
     for (int q = 0; q < 5; q++) part[q] = tot[q] - C[q * RN + (int64_t)r * P.Nc + c];
-    moments(part[0], part[1], part[2], part[3], part[4], fnum_vc, (double)(P.R - 1), loo);
+    moments(part[0], part[1], part[2], part[3], part[4], fnum_vc, (double)(P.R - 1) * m, loo);
     for (int q = 0; q < 5; q++) { const double d = loo[q] - mean[q]; ss[q] += d * d; }
   }
   for (int q = 0; q < 5; q++) o[5 + q] = sqrt((double)(P.R - 1) / (double)P.R * ss[q]);
@@ -1918,14 +1929,14 @@ void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
   hook.after(KSLOT_STEP_END);
 }
 
-void issue_sample(const Prm& P, int slot, cudaStream_t st) {
+void issue_sample(const Prm& P, int slot, int add, cudaStream_t st) {
   launch_zero(P.cell, (int64_t)P.R * P.Nc, st);
   launch_motion(P, 1, st);
   launch_scan(P.cell, (int64_t)P.R * P.Nc, P.scan_part, st, LaunchHook{});
   launch_scatter(P, st);
-  launch_collide(P, 1, slot, st);
-  launch_collide_heavy(P, 1, slot, st);
-  launch_step_end(P, 1, slot, st);
+  launch_collide(P, add ? 2 : 1, slot, st);
+  launch_collide_heavy(P, add ? 2 : 1, slot, st);
+  launch_step_end(P, add ? 2 : 1, slot, st);
 }
 
 const char* kernel_slot_name(int k) {

@@ -40,7 +40,7 @@ void launch_macros(const Prm& P, int slot, double fnum_vc, cudaStream_t st);
 void launch_selftest_philox(int64_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out,
                             uint32_t* out_ref, cudaStream_t st);
 void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook);
-void issue_sample(const Prm& P, int slot, cudaStream_t st);
+void issue_sample(const Prm& P, int slot, int add, cudaStream_t st);
 const char* kernel_slot_name(int k);
 
 }  // namespace dsmc

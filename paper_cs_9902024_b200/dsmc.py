@@ -97,6 +97,8 @@ SIGNATURES = [
     ("dsmc_generate", C.c_int, [_VP]),
     ("dsmc_step", C.c_int, [_VP, C.c_int32]),
     ("dsmc_sample", C.c_int, [_VP, C.c_int32]),
+    ("dsmc_sample_add", C.c_int, [_VP, C.c_int32]),
+    ("dsmc_slot_samples", C.c_int, [_VP, C.c_int32, _VP]),
     ("dsmc_read_macros", C.c_int, [_VP, C.c_int32, _VP]),
     ("dsmc_read_sums", C.c_int, [_VP, C.c_int32, _VP]),
     ("dsmc_status", C.c_int, [_VP, _VP]),
@@ -213,6 +215,22 @@ class Simulation:
 
     def sample(self, slot):
         _check(load_library().dsmc_sample(self.h, int(slot)))
+
+    def sample_add(self, slot):
+        """Time averaging (steady problems): add the current state to the slot."""
+        _check(load_library().dsmc_sample_add(self.h, int(slot)))
+
+    def slot_samples(self, slot):
+        n = C.c_int32(0)
+        _check(load_library().dsmc_slot_samples(self.h, int(slot), C.byref(n)))
+        return n.value
+
+    def time_average(self, slot, n_samples, every):
+        """Steady flow: n_samples samples of the current run state, `every` steps apart,
+        accumulated in `slot` (the unsteady schedule keeps writing its own slots)."""
+        for _ in range(int(n_samples)):
+            self.step(every)
+            self.sample_add(slot)
 
     def read_macros(self, slot):
         out = np.zeros((self.Nc, 10), np.float64)

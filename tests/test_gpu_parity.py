@@ -403,3 +403,29 @@ def test_static_cell_mapping_equals_heavy_queue(dsmc_gpu, monkeypatch):
         sa, sb = a.get_state(r), b.get_state(r)
         for k in sa:
             assert np.array_equal(sa[k], sb[k]), k
+
+
+def test_time_average_matches_oracle(dsmc_gpu, oracle_mod):
+    """Steady-flow time averaging (dsmc_sample_add): accumulated
+    sums and the macros of the averaged slot agree with the oracle's."""
+    p = configs.get("c2_small", n_steps=60)
+    slot = configs.n_slots(p) - 1
+    sim = dsmc_gpu.Simulation(p)
+    sim.generate()
+    sim.step(10)
+    sim.time_average(slot, 5, 3)
+    assert sim.slot_samples(slot) == 5
+    refs = [oracle_mod.OracleRun(p, r) for r in range(p["n_runs"])]
+    for o in refs:
+        o.fill()
+        o.step(10)
+        for _ in range(5):
+            o.step(3)
+            o.sample_add(slot)
+    sums = np.array([o.get_snap(slot) for o in refs])
+    g = sim.read_sums(slot)
+    assert np.allclose(g, sums.transpose(1, 0, 2), rtol=1e-6, atol=1e-5)
+    om = oracle_mod.ensemble(sums, p["fnum_vc"], 5)
+    gm = sim.read_macros(slot)
+    ok = np.isfinite(om)
+    assert np.allclose(gm[ok], om[ok], rtol=1e-6, atol=1e-6)

@@ -534,3 +534,53 @@ def test_run_deterministic(oracle_mod):
     sa, sb = a.get_state(), b.get_state()
     for k in sa:
         assert (sa[k] == sb[k]).all()
+
+
+def test_time_average_accumulates_snapshots(oracle_mod):
+    """Steady problems (NEXT-4): sample_add accumulates exactly the
+    snapshot sums a separate run takes at the same moments, in order, and counts them."""
+    p = configs.get("c4_small", n_steps=40)
+    a = oracle_mod.OracleRun(p, 1)
+    b = oracle_mod.OracleRun(p, 1)
+    a.fill()
+    b.fill()
+    slot = configs.n_slots(p) - 1
+    acc = np.zeros((5, a.Nc))
+    for _ in range(6):
+        a.step(3)
+        b.step(3)
+        a.sample_add(slot)
+        b.sample(0)
+        acc = acc + b.get_snap(0)
+    assert a.snap_count(slot) == 6
+    assert np.array_equal(a.get_snap(slot), acc)
+    a.sample(slot)                       # a snapshot overwrites: count back to 1
+    assert a.snap_count(slot) == 1
+
+
+def test_time_average_estimators(oracle_mod):
+    """Density of a time average of m samples = mean of the m snapshot densities
+    (S_N F_N/V_c/(n m)); in a closed box its mean over cells is the exact particle
+    count per cell; averaging shrinks the cell-to-cell density scatter."""
+    p = configs.get("c4_small", n_steps=200)
+    m, every = 25, 4
+    runs = [oracle_mod.OracleRun(p, r) for r in range(2)]
+    snaps = [[] for _ in runs]
+    acc = []
+    for o, sn in zip(runs, snaps):
+        o.fill()
+        for _ in range(m):
+            o.step(every)
+            o.sample(0)
+            sn.append(o.get_snap(0))
+        acc.append(np.sum(sn, axis=0))
+    fv = p["fnum_vc"]
+    avg = oracle_mod.ensemble(np.array(acc), fv, m)
+    inst = [oracle_mod.ensemble(np.array([sn[k] for sn in snaps]), fv) for k in range(m)]
+    assert np.allclose(avg[:, 0], np.mean([e[:, 0] for e in inst], axis=0), rtol=1e-12)
+    Nc = configs.n_cells(p)
+    n_tot = sum(o.n for o in runs)
+    assert math.isclose(avg[:, 0].mean(), n_tot * fv / (2 * Nc), rel_tol=1e-12)
+    sd_inst = np.mean([e[:, 0].std() for e in inst])
+    assert avg[:, 0].std() < 0.5 * sd_inst, (avg[:, 0].std(), sd_inst)
+    assert abs(np.nanmean(avg[:, 4]) - 1.0) < 0.01      # equilibrium temperature
