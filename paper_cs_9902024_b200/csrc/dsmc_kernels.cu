@@ -1409,7 +1409,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
 constexpr int HT = 256;     // threads per heavy block
 constexpr int CCH = 1024;   // pre-drawn candidates per round
 
-__host__ __device__ inline size_t heavy_smem_bytes(int caph) { return (size_t)caph * 20 + (size_t)CCH * 18 + 16; }
+__host__ __device__ inline size_t heavy_smem_bytes(int caph) { return (size_t)caph * 20 + (size_t)CCH * 25 + 32; }
 
 template <int D>
 __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_arg, int caph) {
@@ -1425,14 +1425,18 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
   float* s_cq = s_cp + CCH;
   uint16_t* s_lw = reinterpret_cast<uint16_t*>(s_cq + CCH);   // last wave that touched a particle
   uint16_t* s_cw = s_lw + caph;                                  // wave of a candidate
-  uint8_t* s_cell = reinterpret_cast<uint8_t*>(s_cw + CCH);
+  uint16_t* s_wl = s_cw + CCH;                                  // candidates in wave order
+  uint32_t* s_wh = reinterpret_cast<uint32_t*>(s_wl + CCH + 2);  // [CCH] per-wave counts -> ends
+  uint8_t* s_clo = reinterpret_cast<uint8_t*>(s_wh + CCH);      // owner cell (lane) of a candidate
+  uint8_t* s_cell = s_clo + CCH;
   uint8_t* s_mod = s_cell + caph;
   __shared__ uint32_t c_st[33], c_N[32], c_M[32], c_mst[33], c_c[32], c_base[32], c_nacc[32];
   __shared__ float c_mg2[32];
   __shared__ uint32_t s_wmax;
   __shared__ int c_r[32], c_h[32], c_reo[32];
   __shared__ float c_gm[32];
-  __shared__ uint32_t s_tile;
+  __shared__ double c_gh[32];
+  __shared__ uint32_t s_tile, s_hwarp[32];
   const int t = threadIdx.x;
   const int64_t RN = (int64_t)P.R * P.Nc;
   const int64_t RS = (int64_t)P.R * P.stride;
@@ -1480,6 +1484,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
       c_h[t] = h;
       c_reo[t] = reo;
       c_gm[t] = gm;
+      c_gh[t] = (double)gm / P.sigma_c;
     }
     __syncthreads();
     int last = 31;
@@ -1500,7 +1505,8 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
         s_cell[q] = (uint8_t)lo;
       }
       __syncthreads();
-      // ---- C: rank of every element inside its segment
+      // ---- C: rank of every element inside its segment (a block bitonic sort of the
+      // tile was tried: 91 block barriers per 8192-element tile made it 35% slower)
       for (uint32_t q = t; q < cnt; q += HT) {
         const int cq = s_cell[q];
         const uint32_t b = c_st[cq] - S, n = c_N[cq], v = s_a[q];
@@ -1543,27 +1549,34 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
         }
         __syncthreads();
         const uint32_t tot = c_mst[32];
-        const uint32_t off = t < 32 ? c_st[t] - S : 0u;
         const double gmd = (double)gm;
         if (t < 32) { c_mg2[t] = 0.0f; c_nacc[t] = 0; }
         uint32_t wbase = 0;   // waves are numbered across rounds, so s_lw needs no reset
         for (uint32_t base = 0; base < tot; base += CCH) {
           const uint32_t lim = tot - base < (uint32_t)CCH ? tot - base : (uint32_t)CCH;
           if (t == 0) s_wmax = wbase;
+          // candidates drawn flattened: owner cell, tile-local particle slots, HS
+          // threshold (as in k_collide's E1) and Marsaglia pair
           for (uint32_t q = t; q < lim; q += HT) {
             const uint32_t gq = base + q;
             int lo = 0;
 #pragma unroll
             for (int stp = 16; stp > 0; stp >>= 1)
               if (lo + stp < 32 && c_mst[lo + stp] <= gq) lo += stp;
-            const uint32_t nc = c_N[lo], kq = gq - c_mst[lo];
+            const uint32_t nc = c_N[lo], kq = gq - c_mst[lo], o = c_st[lo] - S;
             const uint2 keyc = run_key(P, c_r[lo]);
             const uint4 w = draw(keyc, c_c[lo], (uint32_t)s, TAG_COLL_PAIR, kq, 0);
             const uint32_t i = lemire(w.x, nc);
             uint32_t j = lemire(w.y, nc - 1);
             if (j >= i) j++;
-            s_cij[q] = i | (j << 16);
-            s_cur[q] = w.z;
+            s_cij[q] = (o + i) | ((o + j) << 16);
+            s_clo[q] = (uint8_t)lo;
+            if (P.model == 0) {
+              const double lhs = u_co_d(w.z) * c_gh[lo];
+              s_cur[q] = __float_as_uint(__double2float_rd(lhs * lhs));
+            } else {
+              s_cur[q] = w.z;
+            }
             marsaglia_pq(keyc, c_c[lo], (uint32_t)s, kq, s_cp[q], s_cq[q]);
           }
           __syncthreads();
@@ -1576,7 +1589,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
             uint32_t wm = wbase;
             for (uint32_t q = a0; q < a1; q++) {
               const uint32_t pr = s_cij[q - base];
-              const uint32_t i = off + (pr & 0xFFFFu), j = off + (pr >> 16);
+              const uint32_t i = pr & 0xFFFFu, j = pr >> 16;
               uint32_t w = s_lw[i] > s_lw[j] ? s_lw[i] : s_lw[j];
               w = (w > wbase ? w : wbase) + 1;
               s_lw[i] = (uint16_t)w;
@@ -1586,24 +1599,61 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
             }
             atomicMax(&s_wmax, wm);
           }
+          for (uint32_t x = t; x < lim; x += HT) s_wh[x] = 0u;
           __syncthreads();
           const uint32_t wend = s_wmax;
-          for (uint32_t wv = wbase + 1; wv <= wend; wv++) {
-            for (uint32_t q = t; q < lim; q += HT) {
-              if (s_cw[q] != wv) continue;
-              const uint32_t gq = base + q;
-              int lo = 0;
+          const uint32_t nw = wend - wbase;            // <= lim
+          // candidates bucketed by wave (counting sort; order inside a wave is free)
+          for (uint32_t q = t; q < lim; q += HT) atomicAdd(&s_wh[s_cw[q] - wbase - 1u], 1u);
+          __syncthreads();
+          {
+            constexpr int PER = CCH / HT;
+            uint32_t v[PER], sum = 0;
 #pragma unroll
-              for (int stp = 16; stp > 0; stp >>= 1)
-                if (lo + stp < 32 && c_mst[lo + stp] <= gq) lo += stp;
-              const uint32_t o = c_st[lo] - S;
-              const double gml = (double)c_gm[lo];
-              SmemCell A{s_vx + o, s_vy + o, s_vz + o, s_mod + o};
-              float mg = 0.0f;
-              uint32_t na = 0;
-              ntc_apply(P, A, gml, gml / P.sigma_c, s_cij + q, s_cur + q, s_cp + q, s_cq + q, 1, mg, na);
-              atomicMax(reinterpret_cast<uint32_t*>(&c_mg2[lo]), __float_as_uint(mg));  // g^2 >= 0: int order
-              if (na) atomicAdd(&c_nacc[lo], na);
+            for (int u = 0; u < PER; u++) {
+              const uint32_t x = (uint32_t)t * PER + u;
+              v[u] = x < nw ? s_wh[x] : 0u;
+              sum += v[u];
+            }
+            uint32_t total;
+            uint32_t run = block_excl_scan(sum, s_hwarp, total);
+#pragma unroll
+            for (int u = 0; u < PER; u++) {
+              const uint32_t x = (uint32_t)t * PER + u;
+              if (x < nw) s_wh[x] = run;
+              run += v[u];
+            }
+          }
+          __syncthreads();
+          for (uint32_t q = t; q < lim; q += HT) s_wl[atomicAdd(&s_wh[s_cw[q] - wbase - 1u], 1u)] = (uint16_t)q;
+          __syncthreads();                             // s_wh[w] is now the end of wave wbase + 1 + w
+          for (uint32_t wv = 0; wv < nw; wv++) {
+            const uint32_t hi = s_wh[wv];
+            for (uint32_t x = (wv ? s_wh[wv - 1] : 0u) + t; x < hi; x += HT) {
+              const uint32_t q = s_wl[x];
+              const uint32_t pr = s_cij[q];
+              const uint32_t i = pr & 0xFFFFu, j = pr >> 16;
+              const int lo = s_clo[q];
+              const float ax = s_vx[i], ay = s_vy[i], az = s_vz[i];
+              const float bx = s_vx[j], by = s_vy[j], bz = s_vz[j];
+              const float dx = ax - bx, dy = ay - by, dz = az - bz;
+              const float g2 = (dx * dx + dy * dy) + dz * dz;
+              atomicMax(reinterpret_cast<uint32_t*>(&c_mg2[lo]), __float_as_uint(g2));  // g^2 >= 0: int order
+              const bool accept = P.model == 0 ? g2 > __uint_as_float(s_cur[q])
+                                               : vhs_accept(P, s_cur[q], (double)c_gm[lo], g2);
+              if (accept) {
+                const float pp = s_cp[q], qq = s_cq[q];
+                const float rho = pp * pp + qq * qq;
+                const float sr = sqrtf(1.0f - rho);
+                const float ex = 2.0f * pp * sr, ey = 2.0f * qq * sr, ez = 1.0f - 2.0f * rho;
+                const float cmx = (ax + bx) * 0.5f, cmy = (ay + by) * 0.5f, cmz = (az + bz) * 0.5f;
+                const float hh = 0.5f * sqrtf(g2);
+                s_vx[i] = cmx + hh * ex; s_vy[i] = cmy + hh * ey; s_vz[i] = cmz + hh * ez;
+                s_vx[j] = cmx - hh * ex; s_vy[j] = cmy - hh * ey; s_vz[j] = cmz - hh * ez;
+                s_mod[i] = 1;
+                s_mod[j] = 1;
+                atomicAdd(&c_nacc[lo], 1u);
+              }
             }
             __syncthreads();
           }
