@@ -8,7 +8,7 @@
  * runs at once (the outer loop (2), becomes a batch axis).
  * The random number generator is "shifted" per run (PAPER.md:113-115,
  * 435-437) by keying a counter-based Philox4x32-10 with (seed, run id).
- * The exact semantics of every step are DESIGN.md readings R1-R18.
+ * The exact semantics of every step are DESIGN.md readings R1-R23.
  *
  * Conventions for every entry point:
  *   - Return value: DSMC_OK (0) or a negative dsmc_rc code.  No C++
@@ -27,6 +27,11 @@
  *     inside that window.  Host arrays passed to the test/checkpoint hooks are
  *     in store order.
  *   - Thread safety: a dsmc_ctx is used by one host thread at a time.
+ *   - Environment switches read by dsmc_create (measurement A/B only; results are
+ *     bit-identical with or without them): DSMC_STATIC_CELLS=1 disables the
+ *     heavy-tile queue (static lane-per-cell mapping, NEXT-1); DSMC_CAPW=<n>
+ *     overrides the warp-tile staging capacity; DSMC_CARVEOUT=<percent> sets the
+ *     collide kernel's preferred shared-memory carveout.
  */
 #ifndef DSMC_H
 #define DSMC_H

@@ -724,7 +724,7 @@ __device__ __forceinline__ void collide_cell(const Prm& P, uint2 key, uint32_t c
 
 // NTC, split for lane efficiency inside k_collide's shared-memory path:
 // ntc_count() draws M for a cell; the pair draws of all candidates of the tile
-// are then computed lane-parallel (E1) and ntc_apply() walks one cell's
+// are then computed lane-parallel (E1) and ntc_apply_pre() walks one cell's
 // candidates in increasing k (E2), exactly the order of collide_cell().
 __device__ __forceinline__ uint32_t ntc_count(const Prm& P, uint2 key, uint32_t c, uint32_t s, uint32_t N, float gmax) {
   if (N < 2) return 0;
@@ -771,43 +771,6 @@ __device__ __forceinline__ void marsaglia_pq(uint2 key, uint32_t c, uint32_t s, 
   qq_out = 0.0f;
 }
 
-// candidates k in [k_lo, k_hi) of one cell, pre-drawn: ij = i | j << 16,
-// ur = raw acceptance word, (pp, qq) = Marsaglia pair
-template <class A>
-__device__ __forceinline__ void ntc_apply(const Prm& P, const A& acc, double gm, double ghat, const uint32_t* ij,
-                                          const uint32_t* ur, const float* cp, const float* cq, uint32_t n,
-                                          float& maxg2, uint32_t& nacc) {
-  for (uint32_t k = 0; k < n; k++) {
-    const uint32_t pr = ij[k];
-    const uint32_t i = pr & 0xFFFFu, j = pr >> 16;
-    float a[3], b[3];
-    acc.ld(i, a);
-    acc.ld(j, b);
-    const float dx = a[0] - b[0], dy = a[1] - b[1], dz = a[2] - b[2];
-    const float g2 = (dx * dx + dy * dy) + dz * dz;
-    maxg2 = g2 > maxg2 ? g2 : maxg2;
-    bool accept;
-    if (P.model == 0) {
-      const double lhs = u_co_d(ur[k]) * ghat;
-      accept = lhs * lhs < (double)g2;
-    } else {
-      accept = vhs_accept(P, ur[k], gm, g2);
-    }
-    if (accept) {
-      const float pp = cp[k], qq = cq[k];
-      const float rho = pp * pp + qq * qq;
-      const float sr = sqrtf(1.0f - rho);
-      const float e[3] = {2.0f * pp * sr, 2.0f * qq * sr, 1.0f - 2.0f * rho};
-      const float cmx = (a[0] + b[0]) * 0.5f, cmy = (a[1] + b[1]) * 0.5f, cmz = (a[2] + b[2]) * 0.5f;
-      const float hh = 0.5f * sqrtf(g2);
-      const float pa[3] = {cmx + hh * e[0], cmy + hh * e[1], cmz + hh * e[2]};
-      const float pb[3] = {cmx - hh * e[0], cmy - hh * e[1], cmz - hh * e[2]};
-      acc.st(i, pa);
-      acc.st(j, pb);
-      nacc++;
-    }
-  }
-}
 
 // candidates of one cell in increasing k with everything velocity-independent
 // drawn ahead (k_collide): ij = i | j << 16; thr = HS threshold F (accept iff
@@ -949,11 +912,11 @@ constexpr int CCW = 128;    // pre-drawn candidates per round per warp
 
 struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
   uint32_t* sorted; uint32_t* a; float* vy; float* vz; uint8_t* cell; uint8_t* mod;
-  uint32_t* cij; uint32_t* cur; float* cp; float* cq; float* ce; float* mg2; uint32_t* nacc;
+  uint32_t* cij; uint32_t* cur; float* cp; float* cq; float* ce;
 };
 
 __host__ __device__ inline size_t warp_smem_bytes(int capw) {
-  return (size_t)capw * 18 + (size_t)CCW * 20 + 32 * 8 + 16;
+  return (size_t)capw * 18 + (size_t)CCW * 20 + 16;
 }
 
 __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
@@ -967,9 +930,7 @@ __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
   w.cp = reinterpret_cast<float*>(w.cur + CCW);
   w.cq = w.cp + CCW;
   w.ce = w.cq + CCW;
-  w.mg2 = w.ce + CCW;
-  w.nacc = reinterpret_cast<uint32_t*>(w.mg2 + 32);
-  w.cell = reinterpret_cast<uint8_t*>(w.nacc + 32);
+  w.cell = reinterpret_cast<uint8_t*>(w.ce + CCW);
   w.mod = w.cell + capw;
   return w;
 }
