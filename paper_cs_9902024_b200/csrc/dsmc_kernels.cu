@@ -987,45 +987,19 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
           } else {
             W.cur[q] = wp[hh].z;
           }
-        }
-      }
-      // Marsaglia pairs (R14): first block drawn above; later blocks only while
-      // some lane's two tries failed, drawn warp-uniformly (no divergent call)
-      float pp[2], qv[2];
-      bool need[2];
-#pragma unroll
-      for (int hh = 0; hh < 2; hh++) {
-        pp[hh] = 2.0f * u_co(wd[hh].x) - 1.0f;
-        qv[hh] = 2.0f * u_co(wd[hh].y) - 1.0f;
-        if (!(pp[hh] * pp[hh] + qv[hh] * qv[hh] < 1.0f)) {
-          pp[hh] = 2.0f * u_co(wd[hh].z) - 1.0f;
-          qv[hh] = 2.0f * u_co(wd[hh].w) - 1.0f;
-        }
-        need[hh] = qq[hh] < lim && !(pp[hh] * pp[hh] + qv[hh] * qv[hh] < 1.0f);
-      }
-#pragma unroll
-      for (int hh = 0; hh < 2; hh++) {
-        for (uint32_t blk = 1; __any_sync(FULL, need[hh]); blk++) {
-          if (blk >= 64) {            // never reached in practice: e = (0, 0, 1)
-            if (need[hh]) { pp[hh] = 0.0f; qv[hh] = 0.0f; need[hh] = false; }
-            continue;
+          // Marsaglia pair: first block drawn above, further blocks only if both tries fail
+          float pp = 2.0f * u_co(wd[hh].x) - 1.0f, qv = 2.0f * u_co(wd[hh].y) - 1.0f;
+          if (!(pp * pp + qv * qv < 1.0f)) {
+            pp = 2.0f * u_co(wd[hh].z) - 1.0f;
+            qv = 2.0f * u_co(wd[hh].w) - 1.0f;
+            if (!(pp * pp + qv * qv < 1.0f))
+              marsaglia_pq_from(UK ? key_u : run_key(P, rc[hh]), cc[hh], s, kq[hh], 1, pp, qv);
           }
-          const uint4 w = draw(UK ? key_u : run_key(P, rc[hh]), cc[hh], s, TAG_COLL_DIR, kq[hh], blk);
-          const float p0 = 2.0f * u_co(w.x) - 1.0f, q0 = 2.0f * u_co(w.y) - 1.0f;
-          const float p1 = 2.0f * u_co(w.z) - 1.0f, q1 = 2.0f * u_co(w.w) - 1.0f;
-          if (need[hh] && p0 * p0 + q0 * q0 < 1.0f) { pp[hh] = p0; qv[hh] = q0; need[hh] = false; }
-          else if (need[hh] && p1 * p1 + q1 * q1 < 1.0f) { pp[hh] = p1; qv[hh] = q1; need[hh] = false; }
-        }
-      }
-#pragma unroll
-      for (int hh = 0; hh < 2; hh++) {
-        const uint32_t q = qq[hh];
-        if (q < lim) {
           // unit vector of R14, drawn ahead of use
-          const float rho = pp[hh] * pp[hh] + qv[hh] * qv[hh];
+          const float rho = pp * pp + qv * qv;
           const float sr = sqrtf(1.0f - rho);
-          W.cp[q] = 2.0f * pp[hh] * sr;
-          W.cq[q] = 2.0f * qv[hh] * sr;
+          W.cp[q] = 2.0f * pp * sr;
+          W.cq[q] = 2.0f * qv * sr;
           W.ce[q] = 1.0f - 2.0f * rho;
         }
       }
@@ -1309,28 +1283,21 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
         float* __restrict__ vxp = (h ? P1 : P0) + 3 * RS;
         float* __restrict__ vyp = vxp + RS;
         float* __restrict__ vzp = vyp + RS;
-        // collided particles compacted by ballots into a list (the candidate
-        // scratch, free after E), then written back by all lanes together:
-        // no divergent branch per particle
-        uint32_t* list = W.cij;
-        uint32_t nl = 0;
-        for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
-          const uint32_t q = q0 + lane;
-          const bool f = q < cnt && W.mod[q];
-          const unsigned bal = __ballot_sync(FULL, f);
-          if (f) list[nl + __popc(bal & ((1u << lane) - 1u))] = q;
-          nl += __popc(bal);
-          if (nl > (uint32_t)CCW - 32 || q0 + 32 >= cnt) {
-            __syncwarp();
-            for (uint32_t x = lane; x < nl; x += 32) {
-              const uint32_t qq = list[x];
-              const uint32_t g = W.sorted[qq];
-              vxp[g] = wvx[qq];
-              vyp[g] = W.vy[qq];
-              vzp[g] = W.vz[qq];
+        // collided flags read four at a time
+        const uint32_t* m32 = reinterpret_cast<const uint32_t*>(W.mod);
+        for (uint32_t w = lane; w < (cnt + 3) / 4; w += 32) {
+          const uint32_t m = m32[w];
+          if (m) {
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+              if (m & (0xFFu << (8 * b))) {
+                const uint32_t q = 4 * w + b;
+                const uint32_t g = W.sorted[q];
+                vxp[g] = wvx[q];
+                vyp[g] = W.vy[q];
+                vzp[g] = W.vz[q];
+              }
             }
-            __syncwarp();
-            nl = 0;
           }
         }
       }
