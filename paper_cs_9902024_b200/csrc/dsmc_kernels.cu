@@ -29,6 +29,7 @@
 namespace dsmc {
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr int DSMC_MODEL_HS = 0, DSMC_MODEL_VHS = 1;   // Prm::model
 
 // ====================================================================== util
 __global__ void k_zero(uint32_t* __restrict__ a, int64_t n) {
@@ -775,7 +776,7 @@ __device__ __forceinline__ void marsaglia_pq(uint2 key, uint32_t c, uint32_t s, 
 // candidates of one cell in increasing k with everything velocity-independent
 // drawn ahead (k_collide): ij = i | j << 16; thr = HS threshold F (accept iff
 // g2 > F) or the raw VHS acceptance word; (ex, ey, ez) the unit vector (R14)
-template <class A>
+template <int MODEL, class A>
 __device__ __forceinline__ void ntc_apply_pre(const Prm& P, const A& acc, double gm, const uint32_t* ij,
                                               const uint32_t* thr, const float* ex, const float* ey, const float* ez,
                                               uint32_t n, float& maxg2, uint32_t& nacc) {
@@ -788,7 +789,7 @@ __device__ __forceinline__ void ntc_apply_pre(const Prm& P, const A& acc, double
     const float dx = a[0] - b[0], dy = a[1] - b[1], dz = a[2] - b[2];
     const float g2 = (dx * dx + dy * dy) + dz * dz;
     maxg2 = g2 > maxg2 ? g2 : maxg2;
-    const bool accept = P.model == 0 ? g2 > __uint_as_float(thr[k])
+    const bool accept = MODEL == DSMC_MODEL_HS ? g2 > __uint_as_float(thr[k])
                                      : vhs_accept(P, thr[k], gm, g2);
     if (accept) {
       const float e[3] = {ex[k], ey[k], ez[k]};
@@ -939,7 +940,7 @@ __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
 // (two per lane per pass: four independent Philox chains in flight); owner
 // cell of a candidate = last lane with prefix mst <= index.  UK: the tile
 // lies in one run, whose key key_u is then warp-uniform.
-template <bool UK>
+template <bool UK, int MODEL>
 __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int lane, uint32_t base, uint32_t lim,
                                             uint32_t mst, uint32_t N, double ghatu, int r, uint32_t c, uint32_t s,
                                             uint2 key_u) {
@@ -979,7 +980,7 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
           uint32_t j = lemire(wp[hh].y, nc[hh] - 1);
           if (j >= i) j++;
           W.cij[q] = i | (j << 16);
-          if (P.model == 0) {
+          if (MODEL == DSMC_MODEL_HS) {
             // HS: accept iff (double)g2 > (u ghat)^2 (R13)  <=>  g2 > F, F the largest
             // float <= (u ghat)^2 -- the same decision as one fp32 compare in the walk
             const double lhs = u_co_d(wp[hh].z) * gq_hat[hh];
@@ -1006,7 +1007,9 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
     }
 }
 
-template <int D, int NET>
+// MODEL: the collision model is a template parameter so that the hard-sphere
+// kernel carries no VHS code (its presence cost 2.4% at c4)
+template <int D, int NET, int MODEL>
 __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_arg, int capw) {
   extern __shared__ __align__(16) uint8_t dsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1247,22 +1250,23 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_
         const uint32_t lim = tot - base < (uint32_t)CCW ? tot - base : (uint32_t)CCW;
         // two candidates per lane per pass: four independent Philox chains in flight
         if (one_run)
-          ntc_predraw<true>(P, W, lane, base, lim, mst, N, ghatu, r, c, (uint32_t)s, run_key(P, r_first));
+          ntc_predraw<true, MODEL>(P, W, lane, base, lim, mst, N, ghatu, r, c, (uint32_t)s, run_key(P, r_first));
         else
-          ntc_predraw<false>(P, W, lane, base, lim, mst, N, ghatu, r, c, (uint32_t)s, run_key(P, r_first));
+          ntc_predraw<false, MODEL>(P, W, lane, base, lim, mst, N, ghatu, r, c, (uint32_t)s, run_key(P, r_first));
         __syncwarp();
         if (Mu) {
           const uint32_t a0 = mstu > base ? mstu : base;
           const uint32_t a1 = mstu + Mu < base + lim ? mstu + Mu : base + lim;
           if (a0 < a1)
-            ntc_apply_pre(P, Au, gmu, W.cij + (a0 - base), W.cur + (a0 - base), W.cp + (a0 - base),
+            ntc_apply_pre<MODEL>(P, Au, gmu, W.cij + (a0 - base), W.cur + (a0 - base), W.cp + (a0 - base),
                           W.cq + (a0 - base), W.ce + (a0 - base), a1 - a0, maxg2, naccu);
         }
         __syncwarp();
       }
       if (valid && M) {
         nacc = naccu;
-        const double sgm = P.model == 0 ? P.sigma_c * sqrt((double)maxg2) : P.sigma_c * pow((double)maxg2, P.omega1);
+        const double sgm = MODEL == DSMC_MODEL_HS ? P.sigma_c * sqrt((double)maxg2)
+                                                  : P.sigma_c * pow((double)maxg2, P.omega1);
         if (sgm > (double)gm) gm = (float)sgm;
       }
     }
@@ -1853,7 +1857,7 @@ void launch_step_mid(const Prm& P, cudaStream_t st) {
   k_step_mid<<<(P.R + 127) / 128, 128, 0, st>>>(P);
 }
 
-template <int D, int NET>
+template <int D, int NET, int MODEL>
 static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t st) {
   const int64_t RN = (int64_t)P.R * P.Nc;
   const int64_t warps = (RN + 31) / 32;
@@ -1861,24 +1865,30 @@ static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t s
   const size_t smem = WPB * warp_smem_bytes(capw);
   static size_t configured = 0;
   if (smem > configured) {
-    cudaFuncSetAttribute(k_collide<D, NET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_collide<D, NET, MODEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (const char* e = getenv("DSMC_CARVEOUT"))   // A/B experiments: shared-memory carveout (percent)
-      cudaFuncSetAttribute(k_collide<D, NET>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
+      cudaFuncSetAttribute(k_collide<D, NET, MODEL>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
     configured = smem;
   }
-  k_collide<D, NET><<<g, WPB * 32, smem, st>>>(P, mode, slot, capw);
+  k_collide<D, NET, MODEL><<<g, WPB * 32, smem, st>>>(P, mode, slot, capw);
+}
+
+template <int D, int NET>
+static void collide_m(const Prm& P, int mode, int slot, int capw, cudaStream_t st) {
+  if (P.model == DSMC_MODEL_HS) collide_t<D, NET, DSMC_MODEL_HS>(P, mode, slot, capw, st);
+  else collide_t<D, NET, DSMC_MODEL_VHS>(P, mode, slot, capw, st);
 }
 
 void launch_collide(const Prm& P, int mode, int slot, cudaStream_t st) {
-  // register sorting network width: 16 for sparse cells, 32 for dense ones
+  // register sorting network width for segments beyond 32: 16 (sparse) or 32 (dense fills)
   const bool wide = P.net_wide != 0;
   const int capw = P.capw;
   if (P.dim == 1) {
-    if (wide) collide_t<1, 32>(P, mode, slot, capw, st); else collide_t<1, 16>(P, mode, slot, capw, st);
+    if (wide) collide_m<1, 32>(P, mode, slot, capw, st); else collide_m<1, 16>(P, mode, slot, capw, st);
   } else if (P.dim == 2) {
-    if (wide) collide_t<2, 32>(P, mode, slot, capw, st); else collide_t<2, 16>(P, mode, slot, capw, st);
+    if (wide) collide_m<2, 32>(P, mode, slot, capw, st); else collide_m<2, 16>(P, mode, slot, capw, st);
   } else {
-    if (wide) collide_t<3, 32>(P, mode, slot, capw, st); else collide_t<3, 16>(P, mode, slot, capw, st);
+    if (wide) collide_m<3, 32>(P, mode, slot, capw, st); else collide_m<3, 16>(P, mode, slot, capw, st);
   }
 }
 

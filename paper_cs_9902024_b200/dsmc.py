@@ -124,7 +124,10 @@ def load_library(path=None):
         if not os.path.exists(path):
             raise DsmcError(-7, f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
         L = C.CDLL(path)
+        ab = "DSMC_LIB" in os.environ     # A/B builds of older commits may lack newer entry points
         for name, res, args in SIGNATURES:
+            if ab and not hasattr(L, name):
+                continue
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
