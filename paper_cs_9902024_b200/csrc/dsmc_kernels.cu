@@ -1009,8 +1009,9 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
 
 // MODEL: the collision model is a template parameter so that the hard-sphere
 // kernel carries no VHS code (its presence cost 2.4% at c4)
-template <int D, int NET, int MODEL>
-__global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode, int slot_arg, int capw) {
+template <int D, int NET, int MODEL, bool STEP>
+__global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int slot_arg, int capw) {
+  const int mode = STEP ? 0 : mode_arg;      // STEP: the kernel of dsmc_step (mode 0) only
   extern __shared__ __align__(16) uint8_t dsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const WarpSmem W = warp_smem(dsm + (size_t)wid * warp_smem_bytes(capw), capw);
@@ -1857,7 +1858,7 @@ void launch_step_mid(const Prm& P, cudaStream_t st) {
   k_step_mid<<<(P.R + 127) / 128, 128, 0, st>>>(P);
 }
 
-template <int D, int NET, int MODEL>
+template <int D, int NET, int MODEL, bool STEP>
 static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t st) {
   const int64_t RN = (int64_t)P.R * P.Nc;
   const int64_t warps = (RN + 31) / 32;
@@ -1865,18 +1866,22 @@ static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t s
   const size_t smem = WPB * warp_smem_bytes(capw);
   static size_t configured = 0;
   if (smem > configured) {
-    cudaFuncSetAttribute(k_collide<D, NET, MODEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_collide<D, NET, MODEL, STEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (const char* e = getenv("DSMC_CARVEOUT"))   // A/B experiments: shared-memory carveout (percent)
-      cudaFuncSetAttribute(k_collide<D, NET, MODEL>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
+      cudaFuncSetAttribute(k_collide<D, NET, MODEL, STEP>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
     configured = smem;
   }
-  k_collide<D, NET, MODEL><<<g, WPB * 32, smem, st>>>(P, mode, slot, capw);
+  k_collide<D, NET, MODEL, STEP><<<g, WPB * 32, smem, st>>>(P, mode, slot, capw);
 }
 
 template <int D, int NET>
 static void collide_m(const Prm& P, int mode, int slot, int capw, cudaStream_t st) {
-  if (P.model == DSMC_MODEL_HS) collide_t<D, NET, DSMC_MODEL_HS>(P, mode, slot, capw, st);
-  else collide_t<D, NET, DSMC_MODEL_VHS>(P, mode, slot, capw, st);
+  if (mode == 0) {
+    if (P.model == DSMC_MODEL_HS) collide_t<D, NET, DSMC_MODEL_HS, true>(P, mode, slot, capw, st);
+    else collide_t<D, NET, DSMC_MODEL_VHS, true>(P, mode, slot, capw, st);
+  } else {   // explicit Sampling: no Interaction, so the model is irrelevant
+    collide_t<D, NET, DSMC_MODEL_HS, false>(P, mode, slot, capw, st);
+  }
 }
 
 void launch_collide(const Prm& P, int mode, int slot, cudaStream_t st) {
