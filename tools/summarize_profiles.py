@@ -42,8 +42,9 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "lts__t_sector_hit_rate.pct", "lts__t_sector_op_write_hit_rate.pct"]
-traffic = {}
-lines.append("\n## ncu --set full (one launch each, non-reorder step)\n")
+traffic, tcount = {}, {}
+lines.append("\n## ncu --set full (one launch of each kernel per captured step; with K = 2 the two captured steps "
+             "are a reorder and a non-reorder step, and `traffic` is their mean)\n")
 lines.append("| kernel | " + " | ".join(w.replace(".sum", "").replace(".avg.pct_of_peak_sustained_elapsed", " %pk")
                                        .replace(".avg.pct_of_peak_sustained_active", " %") for w in want) + " |")
 lines.append("|---|" + "---|" * len(want))
@@ -57,7 +58,9 @@ for r in rr[2:]:
     b = 0.0
     for w in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         b += float(r[h.index(w)]) * scale.get(u[h.index(w)], 1.0)
-    traffic[name.split("<")[0]] = b
+    base = name.split("<")[0]
+    traffic[base] = traffic.get(base, 0.0) + b
+    tcount[base] = tcount.get(base, 0) + 1
 stalls = []
 for r in rr[2:]:
     name = r[h.index("Kernel Name")].split("(")[0].replace("void ", "")
@@ -68,5 +71,8 @@ for r in rr[2:]:
 lines.append("\nTop warp-stall reasons (cycles per issued instruction):\n")
 lines += stalls
 open(out_md, "w").write("\n".join(lines) + "\n")
+traffic = {k: v / tcount[k] for k, v in traffic.items()}
+lines.append("\nMean DRAM bytes per launch (`traffic` of the bench line): " +
+             ", ".join(f"{k} {v / 1e9:.2f} GB" for k, v in traffic.items()))
 json.dump(traffic, open(os.path.join(ROOT, "profiles", f"traffic_{cfg}.json"), "w"), indent=1)
 print("\n".join(lines))
