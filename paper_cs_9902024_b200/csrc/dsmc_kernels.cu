@@ -1007,6 +1007,13 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
     }
 }
 
+// sample slot of this launch: the schedule's (R2: after step s when (s+1) is a
+// multiple of the sampling interval) in mode 0, the caller's otherwise
+__device__ __forceinline__ int sched_slot(const Prm& P, int mode, int32_t s, int slot_arg) {
+  if (mode != 0) return slot_arg;
+  return ((s + 1) % P.sample_every == 0 && (s + 1) / P.sample_every - 1 < P.n_slots) ? (s + 1) / P.sample_every - 1 : -1;
+}
+
 // MODEL: the collision model is a template parameter so that the hard-sphere
 // kernel carries no VHS code (its presence cost 2.4% at c4)
 template <int D, int NET, int MODEL, bool STEP>
@@ -1045,13 +1052,10 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
   const int h = P.ctl.parity[r];
   const int reo = mode == 0 ? P.ctl.reorder[r] : 0;
   const uint32_t rbase = run_lcr_base(P, r);
+  // the step index (device memory: the graph replays) is first needed by the
+  // draws of E; the schedule decision below uses it only at Sampling, so its
+  // load latency hides behind B-D
   const int32_t s = *P.ctl.step;
-  int slot = -1;
-  if (mode == 0) {
-    if ((s + 1) % P.sample_every == 0 && (s + 1) / P.sample_every - 1 < P.n_slots) slot = (s + 1) / P.sample_every - 1;
-  } else {
-    slot = slot_arg;
-  }
   const uint2 key = run_key(P, r);
   uint32_t ncand = 0, nacc = 0;
   if (cnt > (uint32_t)capw && P.heavy_list) {
@@ -1271,6 +1275,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
         if (sgm > (double)gm) gm = (float)sgm;
       }
     }
+    const int slot = sched_slot(P, mode, s, slot_arg);
     if (valid && slot >= 0) sample_cell(P, slot, k, N, SmemCell{wvx + off, W.vy + off, W.vz + off, W.mod + off}, mode == 2);
     __syncwarp();
     // ---- F
@@ -1338,6 +1343,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
     else heap_sort(seg, N);
     GlobCell A{seg, parr(P, h, 3), parr(P, h, 4), parr(P, h, 5)};
     if (mode == 0) collide_cell(P, key, c, (uint32_t)s, N, A, gm, ncand, nacc);
+    const int slot = sched_slot(P, mode, s, slot_arg);
     if (slot >= 0) sample_cell(P, slot, k, N, A, mode == 2);
     if (reo) {
       for (uint32_t i = 0; i < N; i++) {
