@@ -149,7 +149,7 @@ int make_layout(const dsmc_problem* p, int debug, Layout& L) {
   L.c_psteps = o; o = align_up(o + 8 * R, 16);
   L.c_slot = o; o = align_up(o + 4 * (size_t)(s.n_slots > 0 ? s.n_slots : 1), 16);
   L.c_queue = o; o = align_up(o + 8 * 8, 16);
-  L.c_heavy = o; o = align_up(o + 4 * 4, 16);
+  L.c_heavy = o; o = align_up(o + 4 * 2 * dsmc::HEAVY_TIERS, 16);
   s.ctl = o;
   const size_t F = (size_t)p->ny * p->nz;
   o = 0;
@@ -160,7 +160,7 @@ int make_layout(const dsmc_problem* p, int debug, Layout& L) {
   const int64_t Lscan = L.RN > L.Nc ? L.RN : L.Nc;
   L.s_part = o; o = align_up(o + 4 * ((size_t)dsmc::scan_tiles(Lscan) + 1), 256);
   L.s_macros = o; o = align_up(o + 8 * 10 * (size_t)L.Nc, 256);
-  L.s_heavy = o; o = align_up(o + 4 * ((size_t)(L.RN + 31) / 32 + 1), 256);
+  L.s_heavy = o; o = align_up(o + 4 * dsmc::HEAVY_TIERS * ((size_t)(L.RN + 31) / 32 + 1), 256);
   if (debug) {
     L.s_cand = o; o = align_up(o + 8 * (size_t)L.RN, 256);
     L.s_acc = o; o = align_up(o + 4 * (size_t)L.RN, 256);
@@ -335,11 +335,14 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   P.ctl.queue = (unsigned long long*)(ct + L.c_queue);
   P.ctl.heavy = (uint32_t*)(ct + L.c_heavy);
   P.heavy_list = (uint32_t*)(sc + L.s_heavy);
+  P.heavy_stride = (L.RN + 31) / 32 + 1;
   // NEXT-1 A/B: DSMC_STATIC_CELLS=1 disables the heavy-tile queue, so
   // overflowing tiles stay with their warp (lane = cell, global memory): the
   // static mapping against which the TLPDPR-style reallocation is measured
   if (const char* e = std::getenv("DSMC_STATIC_CELLS")) if (std::atoi(e)) P.heavy_list = nullptr;
   P.caph = 8192;
+  P.caph_tier[0] = 4096;      // 2 blocks per SM (a third tier of 1024, register-limited to 2 too, measured slower)
+  P.caph_tier[1] = P.caph;    // 1 block per SM
 
   auto bail = [&](int code) { delete c; return code; };
   std::vector<int32_t> fj, fk;

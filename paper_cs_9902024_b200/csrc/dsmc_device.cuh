@@ -18,6 +18,7 @@ constexpr uint32_t FILL_STEP = 0xFFFFFFFFu;
 constexpr uint32_t DEAD_KEY = 0xFFFFFFFFu;
 constexpr float DEAD_X = -1.0e30f;           // x of a removed, not yet compacted slot
 constexpr int MAX_BOUNCE = 8;
+constexpr int HEAVY_TIERS = 2;               // heavy-tile queues by size (k_collide_heavy)
 constexpr double TWO_PI = 6.283185307179586;
 
 enum { BC_SPECULAR = 0, BC_PERIODIC = 1, BC_DIFFUSE = 2, BC_OUTFLOW = 3, BC_INFLOW = 4 };
@@ -36,7 +37,7 @@ struct Ctl {
   unsigned long long* psteps;    // [R] sum over steps of live particles after Generation
   int32_t* slot_done;        // [n_slots]
   unsigned long long* queue; // [4][2] work-queue cursors (item, blocks done) per persistent kernel
-  uint32_t* heavy;           // [2] heavy-tile queue: count, next
+  uint32_t* heavy;           // [2*HEAVY_TIERS] heavy-tile queues: count, next per size tier
 };
 
 struct Prm {
@@ -92,7 +93,9 @@ struct Prm {
   int32_t net_wide;          // k_collide sorts segments of <= 32 (else 16) in registers
   int32_t capw;              // particles a warp tile (32 cells) stages in shared memory
   int32_t caph;              // particles k_collide_heavy stages per tile
-  uint32_t* heavy_list;      // [R*Nc/32] tiles k_collide handed to k_collide_heavy
+  uint32_t* heavy_list;      // [HEAVY_TIERS][heavy_stride] tiles k_collide handed to k_collide_heavy, by size tier
+  int64_t heavy_stride;      // entries per tier list (R*Nc/32 + 1)
+  int32_t caph_tier[HEAVY_TIERS];   // staging capacity of each tier (the last one is caph)
   int64_t* dbg_cand;         // [R*Nc]
   int32_t* dbg_acc;          // [R*Nc]
   Ctl ctl;

@@ -554,7 +554,7 @@ __device__ __forceinline__ uint32_t run_lcr_base(const Prm& P, int r) {
 
 __global__ void k_step_end(Prm P, int mode, int slot) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r == 0) { P.ctl.heavy[0] = 0; P.ctl.heavy[1] = 0; }   // heavy-tile queue of k_collide
+  if (r < 2 * HEAVY_TIERS) P.ctl.heavy[r] = 0;   // heavy-tile queues of k_collide
   if (mode != 0) {  // explicit sample (1: snapshot, 2: added to the slot's time average)
     if (r == 0) P.ctl.slot_done[slot] = mode == 1 ? 1 : P.ctl.slot_done[slot] + 1;
     return;
@@ -1061,7 +1061,12 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
   if (cnt > (uint32_t)capw && P.heavy_list) {
     // tile too large for the warp's shared memory: hand it to k_collide_heavy
     // (a whole block with a large staging area -- the "heap" of TLPDPR)
-    if (lane == 0) P.heavy_list[atomicAdd(P.ctl.heavy, 1u)] = (uint32_t)(k0 / 32);
+    // (tiered by size: the smaller the staging area, the more blocks per SM)
+    if (lane == 0) {
+      int q = 0;
+      while (q < HEAVY_TIERS - 1 && cnt > (uint32_t)P.caph_tier[q]) q++;
+      P.heavy_list[(int64_t)q * P.heavy_stride + atomicAdd(P.ctl.heavy + 2 * q, 1u)] = (uint32_t)(k0 / 32);
+    }
     return;
   }
   float gm = valid ? P.gmax[k] : 0.0f;
@@ -1384,7 +1389,7 @@ constexpr int CCH = 1024;   // pre-drawn candidates per round
 __host__ __device__ inline size_t heavy_smem_bytes(int caph) { return (size_t)caph * 20 + (size_t)CCH * 25 + 32; }
 
 template <int D>
-__global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_arg, int caph) {
+__global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_arg, int caph, int queue) {
   extern __shared__ __align__(16) uint8_t dsm[];
   uint32_t* s_sorted = reinterpret_cast<uint32_t*>(dsm);
   uint32_t* s_a = s_sorted + caph;
@@ -1420,14 +1425,16 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
   } else {
     slot = slot_arg;
   }
-  const uint32_t n_heavy = *P.ctl.heavy;
+  const uint32_t* const hlist = P.heavy_list + (int64_t)queue * P.heavy_stride;
+  uint32_t* const hctr = P.ctl.heavy + 2 * queue;
+  const uint32_t n_heavy = hctr[0];
   for (;;) {
     __syncthreads();
-    if (t == 0) s_tile = atomicAdd(P.ctl.heavy + 1, 1u);
+    if (t == 0) s_tile = atomicAdd(hctr + 1, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
     if (tile >= n_heavy) break;
-    const int64_t k0 = (int64_t)P.heavy_list[tile] * 32;
+    const int64_t k0 = (int64_t)hlist[tile] * 32;
     // ---- A (thread per cell)
     const bool valid = t < 32 && k0 + t < RN;
     uint32_t N = 0, c = 0;
@@ -1904,21 +1911,31 @@ void launch_collide(const Prm& P, int mode, int slot, cudaStream_t st) {
 }
 
 template <int D>
-static void heavy_t(const Prm& P, int mode, int slot, cudaStream_t st) {
-  const size_t smem = heavy_smem_bytes(P.caph);
+static void heavy_t(const Prm& P, int mode, int slot, int caph, int queue, cudaStream_t st) {
+  const size_t smem = heavy_smem_bytes(caph);
   static size_t configured = 0;
+  static int occ[HEAVY_TIERS] = {0};
   if (smem > configured) {
-    cudaFuncSetAttribute(k_collide_heavy<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = smem;
+    cudaFuncSetAttribute(k_collide_heavy<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)heavy_smem_bytes(8192));
+    configured = heavy_smem_bytes(8192);
   }
-  k_collide_heavy<D><<<num_sms(), HT, smem, st>>>(P, mode, slot, P.caph);
+  if (!occ[queue]) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[queue], k_collide_heavy<D>, HT, smem);
+    if (occ[queue] < 1) occ[queue] = 1;
+  }
+  k_collide_heavy<D><<<num_sms() * occ[queue], HT, smem, st>>>(P, mode, slot, caph, queue);
 }
 
+// the heap of TLPDPR in HEAVY_TIERS sizes: each tier's persistent blocks stage
+// up to caph_tier[q] particles, so the tiers of small heavy tiles run several
+// blocks per SM; tiles beyond the last tier take its global-memory path
 void launch_collide_heavy(const Prm& P, int mode, int slot, cudaStream_t st) {
   if (!P.heavy_list) return;
-  if (P.dim == 1) heavy_t<1>(P, mode, slot, st);
-  else if (P.dim == 2) heavy_t<2>(P, mode, slot, st);
-  else heavy_t<3>(P, mode, slot, st);
+  for (int q = 0; q < HEAVY_TIERS; q++) {
+    if (P.dim == 1) heavy_t<1>(P, mode, slot, P.caph_tier[q], q, st);
+    else if (P.dim == 2) heavy_t<2>(P, mode, slot, P.caph_tier[q], q, st);
+    else heavy_t<3>(P, mode, slot, P.caph_tier[q], q, st);
+  }
 }
 
 void launch_step_end(const Prm& P, int mode, int slot, cudaStream_t st) {
