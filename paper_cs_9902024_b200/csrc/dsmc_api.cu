@@ -43,7 +43,8 @@ struct Layout {
   int64_t Nc, stride, RN;
   int32_t n_face;
   // ctl offsets
-  size_t c_step, c_status, c_nstore, c_parity, c_reorder, c_inserted, c_counters, c_live, c_psteps, c_slot, c_queue, c_heavy;
+  size_t c_step, c_status, c_nstore, c_parity, c_reorder, c_inserted, c_counters, c_live, c_psteps, c_slot, c_queue, c_heavy,
+      c_items;
   // scratch offsets
   size_t s_face_j, s_face_k, s_open, s_kept, s_part, s_macros, s_heavy, s_cand, s_acc;
 };
@@ -149,6 +150,7 @@ int make_layout(const dsmc_problem* p, int debug, Layout& L) {
   L.c_psteps = o; o = align_up(o + 8 * R, 16);
   L.c_slot = o; o = align_up(o + 4 * (size_t)(s.n_slots > 0 ? s.n_slots : 1), 16);
   L.c_queue = o; o = align_up(o + 8 * 8, 16);
+  L.c_items = o; o = align_up(o + 8 * ((size_t)R + 1), 16);
   L.c_heavy = o; o = align_up(o + 4 * 2 * dsmc::HEAVY_TIERS, 16);
   s.ctl = o;
   const size_t F = (size_t)p->ny * p->nz;
@@ -333,6 +335,7 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   P.ctl.psteps = (unsigned long long*)(ct + L.c_psteps);
   P.ctl.slot_done = (int32_t*)(ct + L.c_slot);
   P.ctl.queue = (unsigned long long*)(ct + L.c_queue);
+  P.ctl.items = (int64_t*)(ct + L.c_items);
   P.ctl.heavy = (uint32_t*)(ct + L.c_heavy);
   P.heavy_list = (uint32_t*)(sc + L.s_heavy);
   P.heavy_stride = (L.RN + 31) / 32 + 1;

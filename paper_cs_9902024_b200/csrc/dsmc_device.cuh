@@ -18,7 +18,7 @@ constexpr uint32_t FILL_STEP = 0xFFFFFFFFu;
 constexpr uint32_t DEAD_KEY = 0xFFFFFFFFu;
 constexpr float DEAD_X = -1.0e30f;           // x of a removed, not yet compacted slot
 constexpr int MAX_BOUNCE = 8;
-constexpr int HEAVY_TIERS = 2;               // heavy-tile queues by size (k_collide_heavy)
+constexpr int HEAVY_TIERS = 2;               // heavy-tile queues by size (k_collide_heavy; k_collide picks 0/1)
 constexpr double TWO_PI = 6.283185307179586;
 
 enum { BC_SPECULAR = 0, BC_PERIODIC = 1, BC_DIFFUSE = 2, BC_OUTFLOW = 3, BC_INFLOW = 4 };
@@ -37,6 +37,7 @@ struct Ctl {
   unsigned long long* psteps;    // [R] sum over steps of live particles after Generation
   int32_t* slot_done;        // [n_slots]
   unsigned long long* queue; // [4][2] work-queue cursors (item, blocks done) per persistent kernel
+  int64_t* items;            // [R+1] work items of the particle kernels, prefix over runs (k_items)
   uint32_t* heavy;           // [2*HEAVY_TIERS] heavy-tile queues: count, next per size tier
 };
 

@@ -438,6 +438,40 @@ __device__ __forceinline__ void queue_done(unsigned long long* q) {
   if (threadIdx.x == 0 && atomicAdd(q + 1, 1ull) == gridDim.x - 1) { q[0] = 0; q[1] = 0; }
 }
 
+// work items of the persistent particle kernels: items[r] = sum over runs r' < r
+// of ceil(n_store[r'] / ITEM), items[R] = total -- only the occupied part of each
+// run's window is walked (open systems sized for growth leave most of it empty)
+__global__ void __launch_bounds__(1024) k_items(Prm P) {
+  __shared__ uint32_t s_warp[32];
+  __shared__ int64_t s_carry;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int r0 = 0; r0 < P.R; r0 += 1024) {
+    const int r = r0 + (int)threadIdx.x;
+    const uint32_t v = r < P.R ? (uint32_t)((P.ctl.n_store[r] + ITEM - 1) / ITEM) : 0u;
+    uint32_t total;
+    const uint32_t pre = block_excl_scan(v, s_warp, total);
+    if (r < P.R) P.ctl.items[r] = s_carry + (int64_t)pre;
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry += (int64_t)total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) P.ctl.items[P.R] = s_carry;
+}
+
+// run of work item `item`: the last r with items[r] <= item (empty runs share
+// their successor's start, so the last one is the occupied run)
+__device__ __forceinline__ int item_run(const Prm& P, int64_t item) {
+  const int64_t per = P.ctl.items[1];
+  if (P.ctl.items[P.R] == per * P.R) return (int)(item / per);   // every run holds as many items (closed box)
+  int lo = 0, hi = P.R;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (P.ctl.items[mid] <= item) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
 // Enumeration (reading R11): floor per axis, clamped.
 template <int D>
 __device__ __forceinline__ uint32_t enumerate(const Prm& P, const float x[3], const float v[3], uint32_t kbase) {
@@ -462,14 +496,12 @@ template <int D, bool EV>
 __global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
   const int lane = threadIdx.x & 31;
   const uint32_t s = (uint32_t)*P.ctl.step;
-  const int64_t items_per_run = (P.cap + ITEM - 1) / ITEM;
-  const int64_t n_items = items_per_run * P.R;
+  const int64_t n_items = P.ctl.items[P.R];
   __shared__ int64_t s_item;
   for (int64_t item = queue_next(P.ctl.queue, &s_item); item < n_items; item = queue_next(P.ctl.queue, &s_item)) {
-  const int r = (int)(item / items_per_run);
+  const int r = item_run(P, item);
   const int64_t n = P.ctl.n_store[r];
-  const int64_t ibase = (item - (int64_t)r * items_per_run) * ITEM;
-  if (ibase >= n) continue;
+  const int64_t ibase = (item - P.ctl.items[r]) * ITEM;
   const int h = P.ctl.parity[r];
   const int64_t base = (int64_t)r * P.stride;
   float* X[3];
@@ -585,15 +617,13 @@ __global__ void k_step_end(Prm P, int mode, int slot) {
 __global__ void __launch_bounds__(256) k_scatter(Prm P) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const int64_t items_per_run = (P.cap + ITEM - 1) / ITEM;
-  const int64_t n_items = items_per_run * P.R;
+  const int64_t n_items = P.ctl.items[P.R];
   __shared__ int64_t s_item;
   for (int64_t item = queue_next(P.ctl.queue + 2, &s_item); item < n_items;
        item = queue_next(P.ctl.queue + 2, &s_item)) {
-    const int r = (int)(item / items_per_run);
+    const int r = item_run(P, item);
     const int64_t n = P.ctl.n_store[r];
-    const int64_t ibase = (item - (int64_t)r * items_per_run) * ITEM;
-    if (ibase >= n) continue;
+    const int64_t ibase = (item - P.ctl.items[r]) * ITEM;
     const int64_t base = (int64_t)r * P.stride;
     const uint32_t* K = P.key + base;
     for (int64_t i0w = ibase + (threadIdx.x >> 5) * 128; i0w < ibase + ITEM && i0w < n; i0w += 1024) {
@@ -1063,8 +1093,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
     // (a whole block with a large staging area -- the "heap" of TLPDPR)
     // (tiered by size: the smaller the staging area, the more blocks per SM)
     if (lane == 0) {
-      int q = 0;
-      while (q < HEAVY_TIERS - 1 && cnt > (uint32_t)P.caph_tier[q]) q++;
+      const int q = cnt > (uint32_t)P.caph_tier[0] ? 1 : 0;      // HEAVY_TIERS == 2
       P.heavy_list[(int64_t)q * P.heavy_stride + atomicAdd(P.ctl.heavy + 2 * q, 1u)] = (uint32_t)(k0 / 32);
     }
     return;
@@ -1844,6 +1873,8 @@ void launch_motion(const Prm& P, int mode, cudaStream_t st) {
   }
 }
 
+void launch_items(const Prm& P, cudaStream_t st) { k_items<<<1, 1024, 0, st>>>(P); }
+
 void launch_scatter(const Prm& P, cudaStream_t st) {
   static int occ = 0;
   if (!occ) {
@@ -1957,6 +1988,7 @@ void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
   launch_zero(P.cell, (int64_t)P.R * P.Nc, st);
   hook.after(KSLOT_ZERO);
   launch_inflow(P, st, hook);
+  launch_items(P, st);
   hook.before(KSLOT_MOTION);
   launch_motion(P, 0, st);
   hook.after(KSLOT_MOTION);
@@ -1964,6 +1996,7 @@ void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
   launch_step_mid(P, st);
   hook.after(KSLOT_STEP_MID);
   launch_scan(P.cell, (int64_t)P.R * P.Nc, P.scan_part, st, hook);
+  launch_items(P, st);
   hook.before(KSLOT_SCATTER);
   launch_scatter(P, st);
   hook.after(KSLOT_SCATTER);
@@ -1980,8 +2013,10 @@ void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
 
 void issue_sample(const Prm& P, int slot, int add, cudaStream_t st) {
   launch_zero(P.cell, (int64_t)P.R * P.Nc, st);
+  launch_items(P, st);
   launch_motion(P, 1, st);
   launch_scan(P.cell, (int64_t)P.R * P.Nc, P.scan_part, st, LaunchHook{});
+  launch_items(P, st);
   launch_scatter(P, st);
   launch_collide(P, add ? 2 : 1, slot, st);
   launch_collide_heavy(P, add ? 2 : 1, slot, st);
