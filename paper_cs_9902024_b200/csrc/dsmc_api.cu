@@ -150,7 +150,7 @@ int make_layout(const dsmc_problem* p, int debug, Layout& L) {
   L.c_psteps = o; o = align_up(o + 8 * R, 16);
   L.c_slot = o; o = align_up(o + 4 * (size_t)(s.n_slots > 0 ? s.n_slots : 1), 16);
   L.c_queue = o; o = align_up(o + 8 * 8, 16);
-  L.c_items = o; o = align_up(o + 8 * ((size_t)R + 1), 16);
+  L.c_items = o; o = align_up(o + 8 * ((size_t)R + 2), 16);
   L.c_heavy = o; o = align_up(o + 4 * 2 * dsmc::HEAVY_TIERS, 16);
   s.ctl = o;
   const size_t F = (size_t)p->ny * p->nz;

@@ -37,7 +37,8 @@ struct Ctl {
   unsigned long long* psteps;    // [R] sum over steps of live particles after Generation
   int32_t* slot_done;        // [n_slots]
   unsigned long long* queue; // [4][2] work-queue cursors (item, blocks done) per persistent kernel
-  int64_t* items;            // [R+1] work items of the particle kernels, prefix over runs (k_items)
+  int64_t* items;            // [R+2] work items of the particle kernels: prefix over runs, total, items per
+                             //       run if all runs hold as many (else 0) -- k_items
   uint32_t* heavy;           // [2*HEAVY_TIERS] heavy-tile queues: count, next per size tier
 };
 

@@ -444,11 +444,14 @@ __device__ __forceinline__ void queue_done(unsigned long long* q) {
 __global__ void __launch_bounds__(1024) k_items(Prm P) {
   __shared__ uint32_t s_warp[32];
   __shared__ int64_t s_carry;
-  if (threadIdx.x == 0) s_carry = 0;
+  __shared__ int s_uniform;
+  if (threadIdx.x == 0) { s_carry = 0; s_uniform = 1; }
   __syncthreads();
+  const uint32_t v0 = (uint32_t)((P.ctl.n_store[0] + ITEM - 1) / ITEM);
   for (int r0 = 0; r0 < P.R; r0 += 1024) {
     const int r = r0 + (int)threadIdx.x;
     const uint32_t v = r < P.R ? (uint32_t)((P.ctl.n_store[r] + ITEM - 1) / ITEM) : 0u;
+    if (r < P.R && v != v0) s_uniform = 0;
     uint32_t total;
     const uint32_t pre = block_excl_scan(v, s_warp, total);
     if (r < P.R) P.ctl.items[r] = s_carry + (int64_t)pre;
@@ -456,14 +459,17 @@ __global__ void __launch_bounds__(1024) k_items(Prm P) {
     if (threadIdx.x == 0) s_carry += (int64_t)total;
     __syncthreads();
   }
-  if (threadIdx.x == 0) P.ctl.items[P.R] = s_carry;
+  if (threadIdx.x == 0) {
+    P.ctl.items[P.R] = s_carry;
+    P.ctl.items[P.R + 1] = s_uniform ? (int64_t)v0 : 0;   // items per run when all runs hold as many
+  }
 }
 
 // run of work item `item`: the last r with items[r] <= item (empty runs share
 // their successor's start, so the last one is the occupied run)
 __device__ __forceinline__ int item_run(const Prm& P, int64_t item) {
-  const int64_t per = P.ctl.items[1];
-  if (P.ctl.items[P.R] == per * P.R) return (int)(item / per);   // every run holds as many items (closed box)
+  const int64_t per = P.ctl.items[P.R + 1];
+  if (per > 0) return (int)(item / per);                         // every run holds as many items (closed box)
   int lo = 0, hi = P.R;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;

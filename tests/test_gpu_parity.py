@@ -429,3 +429,32 @@ def test_time_average_matches_oracle(dsmc_gpu, oracle_mod):
     gm = sim.read_macros(slot)
     ok = np.isfinite(om)
     assert np.allclose(gm[ok], om[ok], rtol=1e-6, atol=1e-6)
+
+
+def test_unequal_runs_in_one_batch(dsmc_gpu):
+    """Runs of unequal store length in one batch (work items 10, 5, 15 per run:
+    the total is a multiple of the first run's) match the same runs computed
+    alone, bit for bit -- the per-run work-item table of the particle kernels."""
+    p = configs.get("c4_small", n_runs=3, n_steps=20)
+    p["fill"] = []
+    p["cap_per_run"] = 61440 + 64
+    sizes = [40960, 20480, 61440]
+    states = [inputs.random_state(40 + r, p, n) for r, n in enumerate(sizes)]
+    big = dsmc_gpu.Simulation(p)
+    big.generate()
+    for r, st in enumerate(states):
+        big.set_state(r, st, step=0)
+    big.step(5)
+    rc, _ = big.status()
+    assert rc == 0
+    for r, st in enumerate(states):
+        q = dict(p)
+        q["n_runs"] = 1
+        q["run_id0"] = r
+        one = dsmc_gpu.Simulation(q)
+        one.generate()
+        one.set_state(0, st, step=0)
+        one.step(5)
+        a, b = big.get_state(r), one.get_state(0)
+        for k in a:
+            assert np.array_equal(a[k], b[k]), (r, k)
