@@ -482,6 +482,8 @@ __device__ __forceinline__ int item_run(const Prm& P, int64_t item) {
 template <int D>
 __device__ __forceinline__ uint32_t enumerate(const Prm& P, const float x[3], const float v[3], uint32_t kbase) {
   int32_t ic[3] = {0, 0, 0};
+  // a non-finite velocity is reported as such (it also makes the position non-finite)
+  if (!(isfinite(v[0]) && isfinite(v[1]) && isfinite(v[2]))) latch(P, ST_NONFINITE);
 #pragma unroll
   for (int a = 0; a < D; a++) {
     const int32_t L = axis_n(P, a);
@@ -489,7 +491,6 @@ __device__ __forceinline__ uint32_t enumerate(const Prm& P, const float x[3], co
     int32_t c = x[a] >= 0.0f ? (int32_t)floorf(x[a]) : 0;
     ic[a] = c > L - 1 ? L - 1 : c;
   }
-  if (!(isfinite(v[0]) && isfinite(v[1]) && isfinite(v[2]))) latch(P, ST_NONFINITE);
   return kbase + (uint32_t)(ic[0] + P.nx * (ic[1] + P.ny * ic[2]));
 }
 

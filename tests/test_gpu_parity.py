@@ -458,3 +458,56 @@ def test_unequal_runs_in_one_batch(dsmc_gpu):
         a, b = big.get_state(r), one.get_state(0)
         for k in a:
             assert np.array_equal(a[k], b[k]), (r, k)
+
+
+# ---- failure detection: device faults latch and surface at the next SYNC call
+
+def test_capacity_overflow_latches(dsmc_gpu):
+    """Inflow beyond the per-run capacity: insertions are dropped and DSMC_ECAP (-4)
+    is returned by the next synchronising call (S:91 style fault, R8)."""
+    p = configs.get("c5_small", n_runs=1)
+    p["cap_per_run"] = configs.n_cells(p) * 2 + 4096      # little room above the fill
+    sim = dsmc_gpu.Simulation(p)
+    sim.generate()
+    sim.step(60)
+    rc, st = sim.status(raise_on_fault=False)
+    assert rc == -4, rc
+    assert st[0]["n_store"] <= p["cap_per_run"]
+
+
+def test_nonfinite_velocity_latches(dsmc_gpu):
+    p = configs.get("c4_small", n_runs=1)
+    st = inputs.random_state(3, p, 4096)
+    st["vx"][17] = np.float32("nan")
+    sim = dsmc_gpu.Simulation(p)
+    sim.generate()
+    sim.set_state(0, st, step=0)
+    sim.step(1)
+    rc, _ = sim.status(raise_on_fault=False)
+    assert rc == -6, rc
+    with pytest.raises(dsmc_gpu.DsmcError):
+        sim.status()
+
+
+def test_outside_domain_latches(dsmc_gpu):
+    """A live particle outside the closed box after Motion is an indexing fault:
+    a periodic wrap moves it by one box length only."""
+    p = configs.get("c4_small", n_runs=1)
+    st = inputs.random_state(5, p, 512)
+    st["x"][3] = np.float32(3 * p["nx"] + 0.5)           # three box lengths out
+    st["vx"][3] = np.float32(0.0)
+    sim = dsmc_gpu.Simulation(p)
+    sim.generate()
+    sim.set_state(0, st, step=0)
+    sim.step(1)
+    rc, _ = sim.status(raise_on_fault=False)
+    assert rc == -5, rc
+
+
+def test_unwritten_slot_is_a_schedule_error(dsmc_gpu):
+    p = configs.get("c4_small", n_runs=1)
+    sim = dsmc_gpu.Simulation(p)
+    sim.generate()
+    with pytest.raises(dsmc_gpu.DsmcError) as e:
+        sim.read_macros(configs.n_slots(p) - 1)
+    assert e.value.args[0] == -8 or "ESCHED" in str(e.value) or "slot" in str(e.value)
