@@ -218,6 +218,19 @@ def run_ours(args):
             "share_of_step": round(d["ms"] / step_ms_sum, 3),
             "kernels": {k: {"ms": round(v["ms"], 4), "GB/s": round(v["gbs"], 1) if v["gbs"] else None,
                             "share": round(v["ms"] / step_ms_sum, 3)} for k, v in kern.items()}}
+    # the two phases of the north-star targets, algorithmic bytes over
+    # summed kernel time, against the measured copy peak and the 8 TB/s nominal
+    phases = {}
+    for ph, names in (("motion+sort", ("k_zero", "k_motion", "k_scan_reduce", "k_scan_partials", "k_scan_down",
+                                        "k_scatter")),
+                      ("collide+sample", ("k_collide", "k_collide_heavy"))):
+        ms = sum(kern[k]["ms"] for k in names if k in kern)
+        b = sum(kern[k]["bytes"] or 0 for k in names if k in kern)
+        if ms > 0:
+            gbs = b / (ms / 1e3) / 1e9
+            phases[ph] = {"ms": round(ms, 4), "GB/s": round(gbs, 1), "frac_measured": round(gbs / hbm, 4),
+                          "frac_8TBs": round(gbs / 8000.0, 4)}
+    roof["phases"] = phases
     traffic_path = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(traffic_path):
         try:
