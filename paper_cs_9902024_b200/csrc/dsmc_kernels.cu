@@ -1419,12 +1419,11 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
 // queue k_collide filled.  Same phases and arithmetic as k_collide:
 // block-parallel staging, rank sort, gather and candidate pre-draws; the
 // per-cell candidate walk stays sequential (thread per cell).
-constexpr int HT = 256;     // threads per heavy block
 constexpr int CCH = 1024;   // pre-drawn candidates per round
 
 __host__ __device__ inline size_t heavy_smem_bytes(int caph) { return (size_t)caph * 20 + (size_t)CCH * 25 + 32; }
 
-template <int D>
+template <int D, int HT>   // HT threads per block: 256 (small tier, two blocks per SM) or 512
 __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_arg, int caph, int queue) {
   extern __shared__ __align__(16) uint8_t dsm[];
   uint32_t* s_sorted = reinterpret_cast<uint32_t*>(dsm);
@@ -1449,7 +1448,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
   __shared__ int c_r[32], c_h[32], c_reo[32];
   __shared__ float c_gm[32];
   __shared__ double c_gh[32];
-  __shared__ uint32_t s_tile, s_hwarp[32];
+  __shared__ uint32_t s_tile, s_hwarp[32], c_k[33], s_nmax;
   const int t = threadIdx.x;
   const int64_t RN = (int64_t)P.R * P.Nc;
   const int64_t RS = (int64_t)P.R * P.stride;
@@ -1500,6 +1499,15 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
       c_reo[t] = reo;
       c_gm[t] = gm;
       c_gh[t] = (double)gm / P.sigma_c;
+      // 32-element sort chunks per cell (prefix) and the largest cell, for phase C
+      const uint32_t nch = valid ? (N + 31u) >> 5 : 0u;
+      uint32_t xk = nch;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, xk, o); if (t >= o) xk += y; }
+      c_k[t] = xk - nch;
+      if (t == 31) c_k[32] = xk;
+      const uint32_t nm = __reduce_max_sync(FULL, valid ? N : 0u);
+      if (t == 0) s_nmax = nm;
     }
     __syncthreads();
     int last = 31;
@@ -1520,16 +1528,55 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
         s_cell[q] = (uint8_t)lo;
       }
       __syncthreads();
-      // ---- C: rank of every element inside its segment (a block bitonic sort of the
-      // tile was tried: 91 block barriers per 8192-element tile made it 35% slower)
-      for (uint32_t q = t; q < cnt; q += HT) {
-        const int cq = s_cell[q];
-        const uint32_t b = c_st[cq] - S, n = c_N[cq], v = s_a[q];
-        uint32_t rank = 0;
-        for (uint32_t p = 0; p < n; p++) rank += s_a[b + p] < v ? 1u : 0u;
-        s_sorted[b + rank] = v;
+      // ---- C: sort every cell's segment: a warp bitonic sort of each 32-element
+      // chunk, then merge rounds in which every element finds its place by a
+      // binary search of the partner run (keys are distinct store slots).  An
+      // O(n^2) rank count was 62% of this kernel's instructions at c5; a block
+      // bitonic sort of the whole tile (91 barriers per 8192 elements) was 35%
+      // slower than that.
+      {
+        const uint32_t nmax = s_nmax;
+        int nlev = 0;
+        for (uint32_t L = 32; L < nmax; L <<= 1) nlev++;
+        uint32_t* from = (nlev & 1) ? s_a : s_sorted;   // the last round lands in s_sorted
+        const int ln = t & 31;
+        const uint32_t nchk = c_k[32];
+        for (uint32_t ch = (uint32_t)(t >> 5); ch < nchk; ch += HT / 32) {
+          int lo = 0;
+#pragma unroll
+          for (int stp = 16; stp > 0; stp >>= 1)
+            if (lo + stp < 32 && c_k[lo + stp] <= ch) lo += stp;
+          const uint32_t b = c_st[lo] - S + ((ch - c_k[lo]) << 5), n = c_st[lo] - S + c_N[lo];
+          const bool in = b + ln < n;
+          uint32_t x = in ? s_a[b + ln] : 0xFFFFFFFFu;
+#pragma unroll
+          for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+              const uint32_t y = __shfl_xor_sync(FULL, x, j);
+              x = (((ln & j) == 0) == ((ln & k) == 0)) ? min(x, y) : max(x, y);
+            }
+          if (in) from[b + ln] = x;
+        }
+        __syncthreads();
+        uint32_t* to = from == s_a ? s_sorted : s_a;
+        int lg = 5;
+        for (uint32_t L = 32; L < nmax; L <<= 1, lg++) {
+          for (uint32_t q = t; q < cnt; q += HT) {
+            const int cq = s_cell[q];
+            const uint32_t b = c_st[cq] - S, n = c_N[cq], i = q - b, v = from[q];
+            const uint32_t run = i >> lg, ps = (run ^ 1u) << lg;
+            const uint32_t plen = ps < n ? min(n - ps, L) : 0u;
+            const uint32_t* A = from + b + ps;
+            uint32_t c = 0;
+            for (uint32_t st = L; st > 0; st >>= 1)
+              if (c + st <= plen && A[c + st - 1] < v) c += st;
+            to[b + ((run & ~1u) << lg) + (i & (L - 1)) + c] = v;
+          }
+          __syncthreads();
+          uint32_t* tmp = from; from = to; to = tmp;
+        }
       }
-      __syncthreads();
       // ---- D: gather velocities (and move positions on reorder steps)
       for (uint32_t q = t; q < cnt; q += HT) {
         const int cq = s_cell[q];
@@ -1948,20 +1995,27 @@ void launch_collide(const Prm& P, int mode, int slot, cudaStream_t st) {
   }
 }
 
-template <int D>
+template <int D, int HT>
 static void heavy_t(const Prm& P, int mode, int slot, int caph, int queue, cudaStream_t st) {
   const size_t smem = heavy_smem_bytes(caph);
-  static size_t configured = 0;
-  static int occ[HEAVY_TIERS] = {0};
-  if (smem > configured) {
-    cudaFuncSetAttribute(k_collide_heavy<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)heavy_smem_bytes(8192));
-    configured = heavy_smem_bytes(8192);
+  static bool configured = false;
+  static int occ = 0;
+  if (!configured) {
+    cudaFuncSetAttribute(k_collide_heavy<D, HT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)heavy_smem_bytes(8192));
+    configured = true;
   }
-  if (!occ[queue]) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[queue], k_collide_heavy<D>, HT, smem);
-    if (occ[queue] < 1) occ[queue] = 1;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collide_heavy<D, HT>, HT, smem);
+    if (occ < 1) occ = 1;
   }
-  k_collide_heavy<D><<<num_sms() * occ[queue], HT, smem, st>>>(P, mode, slot, caph, queue);
+  k_collide_heavy<D, HT><<<num_sms() * occ, HT, smem, st>>>(P, mode, slot, caph, queue);
+}
+
+template <int D>
+static void heavy_q(const Prm& P, int mode, int slot, int q, cudaStream_t st) {
+  // the large tier has one block per SM (shared memory): 512 threads hide more latency
+  if (q == 0) heavy_t<D, 256>(P, mode, slot, P.caph_tier[q], q, st);
+  else heavy_t<D, 512>(P, mode, slot, P.caph_tier[q], q, st);
 }
 
 // the heap of TLPDPR in HEAVY_TIERS sizes: each tier's persistent blocks stage
@@ -1970,9 +2024,9 @@ static void heavy_t(const Prm& P, int mode, int slot, int caph, int queue, cudaS
 void launch_collide_heavy(const Prm& P, int mode, int slot, cudaStream_t st) {
   if (!P.heavy_list) return;
   for (int q = 0; q < HEAVY_TIERS; q++) {
-    if (P.dim == 1) heavy_t<1>(P, mode, slot, P.caph_tier[q], q, st);
-    else if (P.dim == 2) heavy_t<2>(P, mode, slot, P.caph_tier[q], q, st);
-    else heavy_t<3>(P, mode, slot, P.caph_tier[q], q, st);
+    if (P.dim == 1) heavy_q<1>(P, mode, slot, q, st);
+    else if (P.dim == 2) heavy_q<2>(P, mode, slot, q, st);
+    else heavy_q<3>(P, mode, slot, q, st);
   }
 }
 
