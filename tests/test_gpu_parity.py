@@ -123,8 +123,9 @@ def test_one_step_parity_heavy_cells(dsmc_gpu, oracle_mod):
     cells = [5, 6, 7, 300, 301, 2000]
     st = inputs.clustered_state(4, p, cells, 700)
     st2 = inputs.clustered_state(5, p, [9], 3000)
+    st3 = inputs.clustered_state(7, p, [40], 6000)      # a lone cell: merge rounds up to 4096
     for k in st:
-        st[k] = np.concatenate([st[k], st2[k]])
+        st[k] = np.concatenate([st[k], st2[k], st3[k]])
     p["cap_per_run"] = len(st["x"]) + 64
     one_step_case(dsmc_gpu, oracle_mod, p, 0, 2, seed_state=st)
 
