@@ -1519,13 +1519,24 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
     uint32_t ncand = 0, nacc = 0;
     if (cnt <= (uint32_t)caph) {
       // ---- B: stage the LCR slice, tag each element with its cell
-      for (uint32_t q = t; q < cnt; q += HT) {
-        s_a[q] = P.lcr[S + q];
-        int lo = 0;
+      // (this and the loops of C and D take four elements per thread at a time:
+      // independent load and search chains overlap)
+      for (uint32_t q0 = t; q0 < cnt; q0 += 4 * HT) {
+        uint32_t v[4];
 #pragma unroll
-        for (int stp = 16; stp > 0; stp >>= 1)
-          if (lo + stp <= last && c_st[lo + stp] <= S + q) lo += stp;
-        s_cell[q] = (uint8_t)lo;
+        for (int u = 0; u < 4; u++) if (q0 + u * HT < cnt) v[u] = P.lcr[S + q0 + u * HT];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const uint32_t q = q0 + u * HT;
+          if (q < cnt) {
+            s_a[q] = v[u];
+            int lo = 0;
+#pragma unroll
+            for (int stp = 16; stp > 0; stp >>= 1)
+              if (lo + stp <= last && c_st[lo + stp] <= S + q) lo += stp;
+            s_cell[q] = (uint8_t)lo;
+          }
+        }
       }
       __syncthreads();
       // ---- C: sort every cell's segment: a warp bitonic sort of each 32-element
@@ -1562,38 +1573,67 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
         uint32_t* to = from == s_a ? s_sorted : s_a;
         int lg = 5;
         for (uint32_t L = 32; L < nmax; L <<= 1, lg++) {
-          for (uint32_t q = t; q < cnt; q += HT) {
-            const int cq = s_cell[q];
-            const uint32_t b = c_st[cq] - S, n = c_N[cq], i = q - b, v = from[q];
-            const uint32_t run = i >> lg, ps = (run ^ 1u) << lg;
-            const uint32_t plen = ps < n ? min(n - ps, L) : 0u;
-            const uint32_t* A = from + b + ps;
-            uint32_t c = 0;
+          for (uint32_t q0 = t; q0 < cnt; q0 += 4 * HT) {
+            uint32_t v[4], c[4], plen[4], a[4], d[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              const uint32_t q = q0 + u * HT;
+              plen[u] = 0u;
+              c[u] = 0u;
+              if (q < cnt) {
+                const int cq = s_cell[q];
+                const uint32_t b = c_st[cq] - S, n = c_N[cq], i = q - b;
+                const uint32_t run = i >> lg, ps = (run ^ 1u) << lg;
+                v[u] = from[q];
+                plen[u] = ps < n ? min(n - ps, L) : 0u;
+                a[u] = b + ps;
+                d[u] = b + ((run & ~1u) << lg) + (i & (L - 1));
+              }
+            }
             for (uint32_t st = L; st > 0; st >>= 1)
-              if (c + st <= plen && A[c + st - 1] < v) c += st;
-            to[b + ((run & ~1u) << lg) + (i & (L - 1)) + c] = v;
+#pragma unroll
+              for (int u = 0; u < 4; u++)
+                if (c[u] + st <= plen[u] && from[a[u] + c[u] + st - 1] < v[u]) c[u] += st;
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+              if (q0 + u * HT < cnt) to[d[u] + c[u]] = v[u];
           }
           __syncthreads();
           uint32_t* tmp = from; from = to; to = tmp;
         }
       }
       // ---- D: gather velocities (and move positions on reorder steps)
-      for (uint32_t q = t; q < cnt; q += HT) {
-        const int cq = s_cell[q];
-        const int hq = c_h[cq];
-        const uint32_t g = s_sorted[q];
-        const float* src = P.P + (int64_t)hq * P.half + g;
-        if (c_reo[cq]) {
-          float* d = P.P + (int64_t)(hq ^ 1) * P.half + (int64_t)c_r[cq] * P.stride + (int64_t)(S + q - c_base[cq]);
+      for (uint32_t q0 = t; q0 < cnt; q0 += 4 * HT) {
+        float vx[4], vy[4], vz[4];
 #pragma unroll
-          for (int a = 0; a < D; a++) d[a * RS] = src[a * RS];
+        for (int u = 0; u < 4; u++) {
+          const uint32_t q = q0 + u * HT;
+          if (q < cnt) {
+            const float* src = P.P + (int64_t)c_h[s_cell[q]] * P.half + s_sorted[q];
+            vx[u] = src[3 * RS];
+            vy[u] = src[4 * RS];
+            vz[u] = src[5 * RS];
+          }
         }
-        const float vx = src[3 * RS], vy = src[4 * RS], vz = src[5 * RS];
-        s_vx[q] = vx;
-        s_vy[q] = vy;
-        s_vz[q] = vz;
-        s_mod[q] = 0;
-        s_lw[q] = 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const uint32_t q = q0 + u * HT;
+          if (q < cnt) {
+            const int cq = s_cell[q];
+            if (c_reo[cq]) {
+              const int hq = c_h[cq];
+              const float* src = P.P + (int64_t)hq * P.half + s_sorted[q];
+              float* d = P.P + (int64_t)(hq ^ 1) * P.half + (int64_t)c_r[cq] * P.stride + (int64_t)(S + q - c_base[cq]);
+#pragma unroll
+              for (int a = 0; a < D; a++) d[a * RS] = src[a * RS];
+            }
+            s_vx[q] = vx[u];
+            s_vy[q] = vy[u];
+            s_vz[q] = vz[u];
+            s_mod[q] = 0;
+            s_lw[q] = 0;
+          }
+        }
       }
       __syncthreads();
       // ---- E: NTC
