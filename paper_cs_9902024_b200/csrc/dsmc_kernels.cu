@@ -1421,7 +1421,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
 // per-cell candidate walk stays sequential (thread per cell).
 constexpr int CCH = 1024;   // pre-drawn candidates per round
 
-__host__ __device__ inline size_t heavy_smem_bytes(int caph) { return (size_t)caph * 20 + (size_t)CCH * 25 + 32; }
+__host__ __device__ inline size_t heavy_smem_bytes(int caph) { return (size_t)caph * 22 + (size_t)CCH * 18 + 32; }
 
 template <int D, int HT>   // HT threads per block: 256 (small tier, two blocks per SM) or 512
 __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_arg, int caph, int queue) {
@@ -1435,20 +1435,17 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
   uint32_t* s_cur = s_cij + CCH;
   float* s_cp = reinterpret_cast<float*>(s_cur + CCH);
   float* s_cq = s_cp + CCH;
-  uint16_t* s_lw = reinterpret_cast<uint16_t*>(s_cq + CCH);   // last wave that touched a particle
-  uint16_t* s_cw = s_lw + caph;                                  // wave of a candidate
-  uint16_t* s_wl = s_cw + CCH;                                  // candidates in wave order
-  uint32_t* s_wh = reinterpret_cast<uint32_t*>(s_wl + CCH + 2);  // [CCH] per-wave counts -> ends
-  uint8_t* s_clo = reinterpret_cast<uint8_t*>(s_wh + CCH);      // owner cell (lane) of a candidate
-  uint8_t* s_cell = s_clo + CCH;
+  uint32_t* s_min = reinterpret_cast<uint32_t*>(s_cq + CCH);   // earliest undone candidate on a particle
+  uint8_t* s_clo = reinterpret_cast<uint8_t*>(s_min + caph);     // owner cell (lane) of a candidate
+  uint8_t* s_done = s_clo + CCH;                                 // 0 undone, 1 ran this round, 2 earlier
+  uint8_t* s_cell = s_done + CCH;
   uint8_t* s_mod = s_cell + caph;
   __shared__ uint32_t c_st[33], c_N[32], c_M[32], c_mst[33], c_c[32], c_base[32], c_nacc[32];
   __shared__ float c_mg2[32];
-  __shared__ uint32_t s_wmax;
   __shared__ int c_r[32], c_h[32], c_reo[32];
   __shared__ float c_gm[32];
   __shared__ double c_gh[32];
-  __shared__ uint32_t s_tile, s_hwarp[32], c_k[33], s_nmax;
+  __shared__ uint32_t s_tile, c_k[33], s_nmax;
   const int t = threadIdx.x;
   const int64_t RN = (int64_t)P.R * P.Nc;
   const int64_t RS = (int64_t)P.R * P.stride;
@@ -1631,7 +1628,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
             s_vy[q] = vy[u];
             s_vz[q] = vz[u];
             s_mod[q] = 0;
-            s_lw[q] = 0;
+            s_min[q] = 0xFFFFFFFFu;
           }
         }
       }
@@ -1653,10 +1650,8 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
         const uint32_t tot = c_mst[32];
         const double gmd = (double)gm;
         if (t < 32) { c_mg2[t] = 0.0f; c_nacc[t] = 0; }
-        uint32_t wbase = 0;   // waves are numbered across rounds, so s_lw needs no reset
         for (uint32_t base = 0; base < tot; base += CCH) {
           const uint32_t lim = tot - base < (uint32_t)CCH ? tot - base : (uint32_t)CCH;
-          if (t == 0) s_wmax = wbase;
           // candidates drawn flattened: owner cell, tile-local particle slots, HS
           // threshold (as in k_collide's E1) and Marsaglia pair
           for (uint32_t q = t; q < lim; q += HT) {
@@ -1682,59 +1677,33 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
             marsaglia_pq(keyc, c_c[lo], (uint32_t)s, kq, s_cp[q], s_cq[q]);
           }
           __syncthreads();
-          // dependency waves (thread per cell, in increasing k): a candidate
-          // runs after every earlier candidate of its cell that shares a particle
-          if (valid && M) {
-            const uint32_t mst = c_mst[t];
-            const uint32_t a0 = mst > base ? mst : base;
-            const uint32_t a1 = mst + M < base + lim ? mst + M : base + lim;
-            uint32_t wm = wbase;
-            for (uint32_t q = a0; q < a1; q++) {
-              const uint32_t pr = s_cij[q - base];
-              const uint32_t i = pr & 0xFFFFu, j = pr >> 16;
-              uint32_t w = s_lw[i] > s_lw[j] ? s_lw[i] : s_lw[j];
-              w = (w > wbase ? w : wbase) + 1;
-              s_lw[i] = (uint16_t)w;
-              s_lw[j] = (uint16_t)w;
-              s_cw[q - base] = (uint16_t)w;
-              wm = w > wm ? w : wm;
-            }
-            atomicMax(&s_wmax, wm);
-          }
-          for (uint32_t x = t; x < lim; x += HT) s_wh[x] = 0u;
+          // dependency rounds: an undone candidate claims both its particles
+          // (atomicMin of its index) and runs once it is the earliest undone
+          // candidate on both.  Candidates that run together touch disjoint
+          // particles, and every candidate runs after all earlier ones of its cell
+          // that share a particle: the result is that of walking each cell's
+          // candidates in increasing k.  (Replaces dependency waves assigned by a
+          // thread per cell, whose serial loop the whole block waited for.)
+          for (uint32_t q = t; q < lim; q += HT) s_done[q] = 0;
           __syncthreads();
-          const uint32_t wend = s_wmax;
-          const uint32_t nw = wend - wbase;            // <= lim
-          // candidates bucketed by wave (counting sort; order inside a wave is free)
-          for (uint32_t q = t; q < lim; q += HT) atomicAdd(&s_wh[s_cw[q] - wbase - 1u], 1u);
-          __syncthreads();
-          {
-            constexpr int PER = CCH / HT;
-            uint32_t v[PER], sum = 0;
-#pragma unroll
-            for (int u = 0; u < PER; u++) {
-              const uint32_t x = (uint32_t)t * PER + u;
-              v[u] = x < nw ? s_wh[x] : 0u;
-              sum += v[u];
-            }
-            uint32_t total;
-            uint32_t run = block_excl_scan(sum, s_hwarp, total);
-#pragma unroll
-            for (int u = 0; u < PER; u++) {
-              const uint32_t x = (uint32_t)t * PER + u;
-              if (x < nw) s_wh[x] = run;
-              run += v[u];
-            }
-          }
-          __syncthreads();
-          for (uint32_t q = t; q < lim; q += HT) s_wl[atomicAdd(&s_wh[s_cw[q] - wbase - 1u], 1u)] = (uint16_t)q;
-          __syncthreads();                             // s_wh[w] is now the end of wave wbase + 1 + w
-          for (uint32_t wv = 0; wv < nw; wv++) {
-            const uint32_t hi = s_wh[wv];
-            for (uint32_t x = (wv ? s_wh[wv - 1] : 0u) + t; x < hi; x += HT) {
-              const uint32_t q = s_wl[x];
+          for (;;) {
+            for (uint32_t q = t; q < lim; q += HT)
+              if (!s_done[q]) {
+                const uint32_t pr = s_cij[q];
+                atomicMin(&s_min[pr & 0xFFFFu], q);
+                atomicMin(&s_min[pr >> 16], q);
+              }
+            __syncthreads();
+            int more = 0;
+            for (uint32_t q = t; q < lim; q += HT) {
+              if (s_done[q]) continue;
               const uint32_t pr = s_cij[q];
               const uint32_t i = pr & 0xFFFFu, j = pr >> 16;
+              if (s_min[i] != q || s_min[j] != q) {
+                more = 1;
+                continue;
+              }
+              s_done[q] = 1;
               const int lo = s_clo[q];
               const float ax = s_vx[i], ay = s_vy[i], az = s_vz[i];
               const float bx = s_vx[j], by = s_vy[j], bz = s_vz[j];
@@ -1757,13 +1726,17 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
                 atomicAdd(&c_nacc[lo], 1u);
               }
             }
+            more = __syncthreads_or(more);
+            // release the claims of this round's undone candidates (and of those that ran)
+            for (uint32_t q = t; q < lim; q += HT)
+              if (s_done[q] < 2) {
+                const uint32_t pr = s_cij[q];
+                s_min[pr & 0xFFFFu] = 0xFFFFFFFFu;
+                s_min[pr >> 16] = 0xFFFFFFFFu;
+                if (s_done[q]) s_done[q] = 2;
+              }
             __syncthreads();
-          }
-          wbase = wend;
-          if (wbase > 60000u) {  // keep the 16-bit wave ids in range: reset between rounds
-            for (uint32_t q = t; q < cnt; q += HT) s_lw[q] = 0;
-            wbase = 0;
-            __syncthreads();
+            if (!more) break;
           }
         }
         if (valid && M) {
