@@ -633,12 +633,26 @@ __global__ void __launch_bounds__(256) k_scatter(Prm P) {
     const int64_t ibase = (item - P.ctl.items[r]) * ITEM;
     const int64_t base = (int64_t)r * P.stride;
     const uint32_t* K = P.key + base;
-    for (int64_t i0w = ibase + (threadIdx.x >> 5) * 128; i0w < ibase + ITEM && i0w < n; i0w += 1024) {
-    uint32_t kk[4], m[4], p0[4];
+    // the next slice's keys are loaded before this slice's returning atomics, so
+    // the HBM latency of one overlaps the L2 atomic latency of the other
+    const int64_t iend = ibase + ITEM < n ? ibase + ITEM : n;
+    uint32_t kn[4];
+    int64_t i0w = ibase + (threadIdx.x >> 5) * 128;
 #pragma unroll
     for (int j = 0; j < 4; j++) {
       const int64_t i = i0w + j * 32 + lane;
-      kk[j] = i < n ? K[i] : DEAD_KEY;
+      kn[j] = i < iend ? K[i] : DEAD_KEY;
+    }
+    for (; i0w < iend; i0w += 1024) {
+    uint32_t kk[4], m[4], p0[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) kk[j] = kn[j];
+    if (i0w + 1024 < iend) {
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int64_t i = i0w + 1024 + j * 32 + lane;
+        kn[j] = i < iend ? K[i] : DEAD_KEY;
+      }
     }
 #pragma unroll
     for (int j = 0; j < 4; j++) m[j] = __match_any_sync(FULL, kk[j]);
