@@ -93,17 +93,53 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_reduce(const uint32_t* __restri
   if (threadIdx.x == 0) part[blockIdx.x] = total;
 }
 
+// one block: each warp scans a contiguous segment of the tile sums 32 at a time
+// (coalesced loads, all issued up front), then the warp totals are scanned
 __global__ void __launch_bounds__(1024) k_scan_partials(uint32_t* __restrict__ part, int64_t nb) {
   __shared__ uint32_t s_warp[32];
-  const int64_t per = (nb + blockDim.x - 1) / blockDim.x;
-  const int64_t b = (int64_t)threadIdx.x * per;
-  uint32_t s = 0;
-  for (int64_t i = 0; i < per; i++) if (b + i < nb) s += part[b + i];
-  uint32_t total;
-  uint32_t run = block_excl_scan(s, s_warp, total);
-  for (int64_t i = 0; i < per; i++)
-    if (b + i < nb) { uint32_t v = part[b + i]; part[b + i] = run; run += v; }
-  if (threadIdx.x == 0) part[nb] = total;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t seg = (nb + 1023) / 1024 * 32;     // elements per warp, a multiple of 32
+  const int64_t b = (int64_t)wid * seg;
+  uint32_t tot = 0;
+  for (int64_t c0 = 0; c0 < seg; c0 += 32 * 16) {
+    uint32_t v[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const int64_t i = b + c0 + u * 32 + lane;
+      v[u] = c0 + u * 32 < seg && i < nb ? part[i] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; u++) tot += __reduce_add_sync(FULL, v[u]);
+  }
+  if (lane == 0) s_warp[wid] = tot;
+  __syncthreads();
+  if (wid == 0) {
+    const uint32_t x = s_warp[lane];
+    uint32_t y = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const uint32_t z = __shfl_up_sync(FULL, y, o); if (lane >= o) y += z; }
+    s_warp[lane] = y - x;                          // exclusive warp offsets
+    if (lane == 31) part[nb] = y;
+  }
+  __syncthreads();
+  uint32_t run = s_warp[wid];
+  for (int64_t c0 = 0; c0 < seg; c0 += 32 * 16) {
+    uint32_t v[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const int64_t i = b + c0 + u * 32 + lane;
+      v[u] = c0 + u * 32 < seg && i < nb ? part[i] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      uint32_t y = v[u];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) { const uint32_t z = __shfl_up_sync(FULL, y, o); if (lane >= o) y += z; }
+      const int64_t i = b + c0 + u * 32 + lane;
+      if (c0 + u * 32 < seg && i < nb) part[i] = run + y - v[u];
+      run += __shfl_sync(FULL, y, 31);
+    }
+  }
 }
 
 __global__ void __launch_bounds__(SCAN_T) k_scan_down(uint32_t* __restrict__ a, int64_t L,
