@@ -297,6 +297,11 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
     // than in the heavy queue (c5 after 500 steps, capw 256 / 512 / 768 / 1024:
     // 3.92 / 3.65 / 3.66 / 3.90 ms per step)
     if (p->inflow_kind == DSMC_INFLOW_EFFUSIVE) capw = std::max(capw, 512);
+    // dense fills (cells beyond the 32-wide register sort, ~100 candidates per cell):
+    // one lane walking a cell's candidates is the bottleneck, and the heavy blocks'
+    // claim rounds walk them in parallel (c2 from the fill, capw 512 / 1024 / 1832:
+    // 0.451 / 0.512 / 0.628 ms per step; c3 at 20 per cell stays faster in the warp path)
+    if (ppc_max > 32) capw = 512;
     if (const char* e = std::getenv("DSMC_CAPW")) capw = std::max(256, std::min(std::atoi(e), 4096));   // A/B experiments
     P.capw = (capw + 31) / 32 * 32;
   }
