@@ -1546,8 +1546,8 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
       c_reo[t] = reo;
       c_gm[t] = gm;
       c_gh[t] = (double)gm / P.sigma_c;
-      // 32-element sort chunks per cell (prefix) and the largest cell, for phase C
-      const uint32_t nch = valid ? (N + 31u) >> 5 : 0u;
+      // 64-element sort chunks per cell (prefix) and the largest cell, for phase C
+      const uint32_t nch = valid ? (N + 63u) >> 6 : 0u;
       uint32_t xk = nch;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, xk, o); if (t >= o) xk += y; }
@@ -1586,7 +1586,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
         }
       }
       __syncthreads();
-      // ---- C: sort every cell's segment: a warp bitonic sort of each 32-element
+      // ---- C: sort every cell's segment: a warp bitonic sort of each 64-element
       // chunk, then merge rounds in which every element finds its place by a
       // binary search of the partner run (keys are distinct store slots).  An
       // O(n^2) rank count was 62% of this kernel's instructions at c5; a block
@@ -1595,7 +1595,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
       {
         const uint32_t nmax = s_nmax;
         int nlev = 0;
-        for (uint32_t L = 32; L < nmax; L <<= 1) nlev++;
+        for (uint32_t L = 64; L < nmax; L <<= 1) nlev++;
         uint32_t* from = (nlev & 1) ? s_a : s_sorted;   // the last round lands in s_sorted
         const int ln = t & 31;
         const uint32_t nchk = c_k[32];
@@ -1604,22 +1604,32 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
 #pragma unroll
           for (int stp = 16; stp > 0; stp >>= 1)
             if (lo + stp < 32 && c_k[lo + stp] <= ch) lo += stp;
-          const uint32_t b = c_st[lo] - S + ((ch - c_k[lo]) << 5), n = c_st[lo] - S + c_N[lo];
-          const bool in = b + ln < n;
-          uint32_t x = in ? s_a[b + ln] : 0xFFFFFFFFu;
+          const uint32_t b = c_st[lo] - S + ((ch - c_k[lo]) << 6), n = c_st[lo] - S + c_N[lo];
+          const bool in0 = b + ln < n, in1 = b + 32 + ln < n;
+          uint32_t x0 = in0 ? s_a[b + ln] : 0xFFFFFFFFu, x1 = in1 ? s_a[b + 32 + ln] : 0xFFFFFFFFu;
+          // 64-element bitonic sort, element e = lane + 32 h in x_h
 #pragma unroll
-          for (int k = 2; k <= 32; k <<= 1)
+          for (int k = 2; k <= 64; k <<= 1)
 #pragma unroll
             for (int j = k >> 1; j > 0; j >>= 1) {
-              const uint32_t y = __shfl_xor_sync(FULL, x, j);
-              x = (((ln & j) == 0) == ((ln & k) == 0)) ? min(x, y) : max(x, y);
+              if (j == 32) {                       // partners in one lane (k == 64: ascending)
+                const uint32_t lo_ = min(x0, x1), hi_ = max(x0, x1);
+                x0 = lo_;
+                x1 = hi_;
+              } else {
+                const uint32_t y0 = __shfl_xor_sync(FULL, x0, j), y1 = __shfl_xor_sync(FULL, x1, j);
+                const bool lower = (ln & j) == 0;
+                x0 = (lower == ((ln & k) == 0)) ? min(x0, y0) : max(x0, y0);
+                x1 = (lower == (((ln + 32) & k) == 0)) ? min(x1, y1) : max(x1, y1);
+              }
             }
-          if (in) from[b + ln] = x;
+          if (in0) from[b + ln] = x0;
+          if (in1) from[b + 32 + ln] = x1;
         }
         __syncthreads();
         uint32_t* to = from == s_a ? s_sorted : s_a;
-        int lg = 5;
-        for (uint32_t L = 32; L < nmax; L <<= 1, lg++) {
+        int lg = 6;
+        for (uint32_t L = 64; L < nmax; L <<= 1, lg++) {
           for (uint32_t q0 = t; q0 < cnt; q0 += 4 * HT) {
             uint32_t v[4], c[4], plen[4], a[4], d[4];
 #pragma unroll
