@@ -1710,6 +1710,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
         const uint32_t tot = c_mst[32];
         const double gmd = (double)gm;
         if (t < 32) { c_mg2[t] = 0.0f; c_nacc[t] = 0; }
+        uint32_t rnd = 0;                          // claim rounds so far in this tile
         for (uint32_t base = 0; base < tot; base += CCH) {
           const uint32_t lim = tot - base < (uint32_t)CCH ? tot - base : (uint32_t)CCH;
           // candidates drawn flattened: owner cell, tile-local particle slots, HS
@@ -1744,14 +1745,18 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
           // that share a particle: the result is that of walking each cell's
           // candidates in increasing k.  (Replaces dependency waves assigned by a
           // thread per cell, whose serial loop the whole block waited for.)
+          // A claim is (0xFFFF - round) << 16 | q: a later round's claims beat any
+          // left from earlier rounds, so claims need no release pass.
           for (uint32_t q = t; q < lim; q += HT) s_done[q] = 0;
           __syncthreads();
           for (;;) {
+            const uint32_t rtag = (0xFFFFu - rnd) << 16;
+            rnd++;
             for (uint32_t q = t; q < lim; q += HT)
               if (!s_done[q]) {
                 const uint32_t pr = s_cij[q];
-                atomicMin(&s_min[pr & 0xFFFFu], q);
-                atomicMin(&s_min[pr >> 16], q);
+                atomicMin(&s_min[pr & 0xFFFFu], rtag | q);
+                atomicMin(&s_min[pr >> 16], rtag | q);
               }
             __syncthreads();
             int more = 0;
@@ -1759,7 +1764,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
               if (s_done[q]) continue;
               const uint32_t pr = s_cij[q];
               const uint32_t i = pr & 0xFFFFu, j = pr >> 16;
-              if (s_min[i] != q || s_min[j] != q) {
+              if (s_min[i] != (rtag | q) || s_min[j] != (rtag | q)) {
                 more = 1;
                 continue;
               }
@@ -1787,15 +1792,11 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
               }
             }
             more = __syncthreads_or(more);
-            // release the claims of this round's undone candidates (and of those that ran)
-            for (uint32_t q = t; q < lim; q += HT)
-              if (s_done[q] < 2) {
-                const uint32_t pr = s_cij[q];
-                s_min[pr & 0xFFFFu] = 0xFFFFFFFFu;
-                s_min[pr >> 16] = 0xFFFFFFFFu;
-                if (s_done[q]) s_done[q] = 2;
-              }
-            __syncthreads();
+            if (rnd > 0xFFF0u) {                       // round tags nearly exhausted: reset the claims
+              for (uint32_t q = t; q < cnt; q += HT) s_min[q] = 0xFFFFFFFFu;
+              rnd = 0;
+              __syncthreads();
+            }
             if (!more) break;
           }
         }
