@@ -130,6 +130,20 @@ def test_one_step_parity_heavy_cells(dsmc_gpu, oracle_mod):
     one_step_case(dsmc_gpu, oracle_mod, p, 0, 2, seed_state=st)
 
 
+def test_one_step_parity_heavy_chunk_edges(dsmc_gpu, oracle_mod):
+    """Heavy-tile segment sort at its chunk and merge-round edges: one 32-cell tile
+    whose cells hold 1, 63, 64, 65, 127, 128, 129, 255, 256, 257 and 511 particles
+    (64-element warp chunks, merge rounds of 64..256, a ragged last chunk)."""
+    p = configs.get("c4_small")
+    p["reorder_every"] = 1
+    p["fill"] = []
+    sizes = [1, 63, 64, 65, 127, 128, 129, 255, 256, 257, 511]
+    parts = [inputs.clustered_state(20 + k, p, [32 * 3 + 2 * k], n) for k, n in enumerate(sizes)]
+    st = {k: np.concatenate([q[k] for q in parts]) for k in parts[0]}
+    p["cap_per_run"] = len(st["x"]) + 64
+    one_step_case(dsmc_gpu, oracle_mod, p, 0, 2, seed_state=st)
+
+
 def test_one_step_parity_giant_cell(dsmc_gpu, oracle_mod):
     """A cell beyond even the heavy staging area (9000 > 8192 particles):
     the per-thread global-memory fallback of k_collide_heavy."""
