@@ -1471,7 +1471,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
 // per-cell candidate walk stays sequential (thread per cell).
 constexpr int CCH = 1024;   // pre-drawn candidates per round
 
-__host__ __device__ inline size_t heavy_smem_bytes(int caph) { return (size_t)caph * 22 + (size_t)CCH * 18 + 32; }
+__host__ __device__ inline size_t heavy_smem_bytes(int caph) { return (size_t)caph * 22 + (size_t)CCH * 17 + 32; }
 
 template <int D, int HT>   // HT threads per block: 256 (small tier, two blocks per SM) or 512
 __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_arg, int caph, int queue) {
@@ -1487,8 +1487,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
   float* s_cq = s_cp + CCH;
   uint32_t* s_min = reinterpret_cast<uint32_t*>(s_cq + CCH);   // earliest undone candidate on a particle
   uint8_t* s_clo = reinterpret_cast<uint8_t*>(s_min + caph);     // owner cell (lane) of a candidate
-  uint8_t* s_done = s_clo + CCH;                                 // 0 undone, 1 ran this round, 2 earlier
-  uint8_t* s_cell = s_done + CCH;
+  uint8_t* s_cell = s_clo + CCH;
   uint8_t* s_mod = s_cell + caph;
   __shared__ uint32_t c_st[33], c_N[32], c_M[32], c_mst[33], c_c[32], c_base[32], c_nacc[32];
   __shared__ float c_mg2[32];
@@ -1747,28 +1746,29 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
           // thread per cell, whose serial loop the whole block waited for.)
           // A claim is (0xFFFF - round) << 16 | q: a later round's claims beat any
           // left from earlier rounds, so claims need no release pass.
-          for (uint32_t q = t; q < lim; q += HT) s_done[q] = 0;
-          __syncthreads();
+          // each thread owns candidates t + u HT; which are undone is a register mask
+          constexpr int OWN = CCH / HT;
+          uint32_t undone = 0;
+#pragma unroll
+          for (int u = 0; u < OWN; u++) if (t + u * HT < lim) undone |= 1u << u;
           for (;;) {
             const uint32_t rtag = (0xFFFFu - rnd) << 16;
             rnd++;
-            for (uint32_t q = t; q < lim; q += HT)
-              if (!s_done[q]) {
-                const uint32_t pr = s_cij[q];
+#pragma unroll
+            for (int u = 0; u < OWN; u++)
+              if (undone >> u & 1u) {
+                const uint32_t q = t + u * HT, pr = s_cij[q];
                 atomicMin(&s_min[pr & 0xFFFFu], rtag | q);
                 atomicMin(&s_min[pr >> 16], rtag | q);
               }
             __syncthreads();
-            int more = 0;
-            for (uint32_t q = t; q < lim; q += HT) {
-              if (s_done[q]) continue;
-              const uint32_t pr = s_cij[q];
+#pragma unroll
+            for (int u = 0; u < OWN; u++) {
+              if (!(undone >> u & 1u)) continue;
+              const uint32_t q = t + u * HT, pr = s_cij[q];
               const uint32_t i = pr & 0xFFFFu, j = pr >> 16;
-              if (s_min[i] != (rtag | q) || s_min[j] != (rtag | q)) {
-                more = 1;
-                continue;
-              }
-              s_done[q] = 1;
+              if (s_min[i] != (rtag | q) || s_min[j] != (rtag | q)) continue;
+              undone &= ~(1u << u);
               const int lo = s_clo[q];
               const float ax = s_vx[i], ay = s_vy[i], az = s_vz[i];
               const float bx = s_vx[j], by = s_vy[j], bz = s_vz[j];
@@ -1791,6 +1791,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
                 atomicAdd(&c_nacc[lo], 1u);
               }
             }
+            int more = undone != 0u;
             more = __syncthreads_or(more);
             if (rnd > 0xFFF0u) {                       // round tags nearly exhausted: reset the claims
               for (uint32_t q = t; q < cnt; q += HT) s_min[q] = 0xFFFFFFFFu;
