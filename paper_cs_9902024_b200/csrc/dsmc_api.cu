@@ -354,7 +354,7 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   // static mapping against which the TLPDPR-style reallocation is measured
   if (const char* e = std::getenv("DSMC_STATIC_CELLS")) if (std::atoi(e)) P.heavy_list = nullptr;
   P.caph = 8192;
-  P.caph_tier[0] = 4096;      // 2 blocks per SM (a third tier of 1024, register-limited to 2 too, measured slower)
+  P.caph_tier[0] = 3584;      // 2 blocks per SM within the 196 KB carveout (4096: 215 KB, L1 down to 28 KB, 2-3% slower; a third tier of 1024, register-limited to 2 blocks too, measured slower)
   P.caph_tier[1] = P.caph;    // 1 block per SM
 
   auto bail = [&](int code) { delete c; return code; };
