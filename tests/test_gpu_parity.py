@@ -528,3 +528,27 @@ def test_unwritten_slot_is_a_schedule_error(dsmc_gpu):
     with pytest.raises(dsmc_gpu.DsmcError) as e:
         sim.read_macros(configs.n_slots(p) - 1)
     assert e.value.args[0] == -8 or "ESCHED" in str(e.value) or "slot" in str(e.value)
+
+
+@pytest.mark.parametrize("name,steps", [("c2_small", 12), ("c5_small", 30)])
+def test_staging_capacity_does_not_change_results(dsmc_gpu, monkeypatch, name, steps):
+    """Which tiles take the warp path and which the heavy blocks (DSMC_CAPW, the
+    per-config staging rule of DESIGN section 4) changes time, never answers."""
+    def run(capw):
+        if capw:
+            monkeypatch.setenv("DSMC_CAPW", str(capw))
+        else:
+            monkeypatch.delenv("DSMC_CAPW", raising=False)
+        p = configs.get(name)
+        sim = dsmc_gpu.Simulation(p)
+        sim.generate()
+        sim.step(steps)
+        return sim, p
+    ref, p = run(None)
+    for capw in (256, 4096):
+        sim, _ = run(capw)
+        assert sim.status()[1] == ref.status()[1]
+        for r in range(p["n_runs"]):
+            sa, sb = sim.get_state(r), ref.get_state(r)
+            for k in sa:
+                assert np.array_equal(sa[k], sb[k]), (capw, r, k)
