@@ -1629,30 +1629,48 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
         uint32_t* to = from == s_a ? s_sorted : s_a;
         int lg = 6;
         for (uint32_t L = 64; L < nmax; L <<= 1, lg++) {
-          for (uint32_t q0 = t; q0 < cnt; q0 += 4 * HT) {
-            uint32_t v[4], c[4], plen[4], a[4], d[4];
+          // merge path: each thread writes MV consecutive outputs; it locates the
+          // split of its first output in the run pair by a binary search along the
+          // diagonal, then merges sequentially (again where a pair or segment ends)
+          constexpr uint32_t MV = 8;
+          for (uint32_t g0 = t * MV; g0 < cnt; g0 += HT * MV) {
+            uint32_t cur = 0xFFFFFFFFu, la = 0, lb = 0, ai = 0, bi = 0, va = 0, vb = 0;
+            const uint32_t* A = from;
+            const uint32_t* B = from;
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-              const uint32_t q = q0 + u * HT;
-              plen[u] = 0u;
-              c[u] = 0u;
-              if (q < cnt) {
-                const int cq = s_cell[q];
-                const uint32_t b = c_st[cq] - S, n = c_N[cq], i = q - b;
-                const uint32_t run = i >> lg, ps = (run ^ 1u) << lg;
-                v[u] = from[q];
-                plen[u] = ps < n ? min(n - ps, L) : 0u;
-                a[u] = b + ps;
-                d[u] = b + ((run & ~1u) << lg) + (i & (L - 1));
+            for (uint32_t u = 0; u < MV; u++) {
+              const uint32_t q = g0 + u;
+              if (q >= cnt) break;
+              const int cq = s_cell[q];
+              const uint32_t b = c_st[cq] - S, n = c_N[cq];
+              const uint32_t off = ((q - b) >> (lg + 1)) << (lg + 1);   // pair start in the segment
+              if (b + off != cur) {
+                cur = b + off;
+                la = min(n - off, L);
+                lb = n - off > L ? min(n - off - L, L) : 0u;
+                A = from + cur;
+                B = A + L;
+                const uint32_t diag = q - cur;
+                uint32_t lo = diag > lb ? diag - lb : 0u, hi = min(diag, la);
+                while (lo < hi) {
+                  const uint32_t mid = (lo + hi) >> 1;
+                  if (A[mid] < B[diag - 1 - mid]) lo = mid + 1; else hi = mid;
+                }
+                ai = lo;
+                bi = diag - lo;
+                va = ai < la ? A[ai] : 0xFFFFFFFFu;
+                vb = bi < lb ? B[bi] : 0xFFFFFFFFu;
+              }
+              if (va < vb) {
+                to[q] = va;
+                ai++;
+                va = ai < la ? A[ai] : 0xFFFFFFFFu;
+              } else {
+                to[q] = vb;
+                bi++;
+                vb = bi < lb ? B[bi] : 0xFFFFFFFFu;
               }
             }
-            for (uint32_t st = L; st > 0; st >>= 1)
-#pragma unroll
-              for (int u = 0; u < 4; u++)
-                if (c[u] + st <= plen[u] && from[a[u] + c[u] + st - 1] < v[u]) c[u] += st;
-#pragma unroll
-            for (int u = 0; u < 4; u++)
-              if (q0 + u * HT < cnt) to[d[u] + c[u]] = v[u];
           }
           __syncthreads();
           uint32_t* tmp = from; from = to; to = tmp;
