@@ -285,7 +285,7 @@ def test_explicit_sample_matches_oracle(dsmc_gpu, oracle_mod):
     assert np.allclose(g, sums.transpose(1, 0, 2), rtol=1e-6, atol=1e-5)
 
 
-@pytest.mark.parametrize("name,warm,run", [("c3", 40, 1), ("c5", 80, 0), ("c2", 30, 3)])
+@pytest.mark.parametrize("name,warm,run", [("c3", 40, 1), ("c5", 80, 0), ("c2", 30, 3), ("c5", 500, 1), ("c2", 200, 2)])
 def test_full_size_sampled_parity(dsmc_gpu, oracle_mod, name, warm, run):
     """Full BASELINE grid and fill in the bench's launch configuration (reduced
     run count): after `warm` GPU steps (c5: the orifice jet has built heavy
@@ -296,10 +296,10 @@ def test_full_size_sampled_parity(dsmc_gpu, oracle_mod, name, warm, run):
     if name == "c3":
         kw["n_steps"] = 100
     if name == "c5":
-        kw["n_steps"] = 100
+        kw["n_steps"] = max(100, (warm // 50 + 1) * 50)     # a multiple of dt_s = 50 dt
         kw["cap_per_run"] = 12 << 20
     if name == "c2":
-        kw["n_steps"] = 40
+        kw["n_steps"] = max(40, (warm // 20 + 1) * 20)      # a multiple of dt_s = 20 dt
     p = configs.get(name, **kw)
     p["dt_s"] = p["dt"] * (20 if name == "c2" else 50)
     sim = dsmc_gpu.Simulation(p, debug=True)
