@@ -710,6 +710,7 @@ __global__ void __launch_bounds__(256) k_scatter(Prm P) {
 // ============================================================= Interaction
 // Isotropic direction, Marsaglia (reading R14)
 __device__ __forceinline__ void marsaglia(uint2 key, uint32_t c, uint32_t s, uint32_t k, float e[3]) {
+#pragma unroll 1
   for (uint32_t blk = 0; blk < 64; blk++) {
     const uint4 w = draw(key, c, s, TAG_COLL_DIR, k, blk);
     const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
@@ -826,6 +827,7 @@ __device__ __forceinline__ uint32_t ntc_count(const Prm& P, uint2 key, uint32_t 
 // Marsaglia pair from block b0 on (the first block is handled inline by k_collide)
 __device__ __noinline__ void marsaglia_pq_from(uint2 key, uint32_t c, uint32_t s, uint32_t k, uint32_t b0,
                                                float& pp_out, float& qq_out) {
+#pragma unroll 1   // cold (both tries of block 0 rejected): keep the code small
   for (uint32_t blk = b0; blk < 64; blk++) {
     const uint4 w = draw(key, c, s, TAG_COLL_DIR, k, blk);
     const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
