@@ -1,5 +1,2 @@
-mkdir -p gpurun_out
-for K in 1 2 4 8; do
-  timeout 300 python bench.py --n-runs 64 --steps 16 --warmup 4 --timed-steps 8 --no-cpu --no-e2e --reorder-every $K > gpurun_out/k$K.log 2>&1
-  echo "K=$K"; python tools/summ_bench.py gpurun_out/k$K.log
-done
+# usage: bash tools/gpu_ksweep.sh -- c4 (n = 256) ms/step per reorder period K
+for K in 1 2 3 4; do timeout 600 python bench.py --steps 12 --warmup 4 --no-cpu --no-e2e --reorder-every $K > gpurun_out/ks$K.log 2>&1; python tools/summ_bench.py gpurun_out/ks$K.log | head -1; done
