@@ -480,12 +480,15 @@ static void indexing(orc_run* R) {
 }
 
 /* ------------------------------------------------------- Interaction -- */
-/* Isotropic unit vector, Marsaglia (1972) (reading R14). */
-static void marsaglia(const orc_run* R, uint32_t c, uint32_t s, uint32_t k, float e[3]) {
-  for (uint32_t blk = 0; blk < 64; blk++) {
-    uint32_t w[4];
-    draw(R, c, s, TAG_COLL_DIR, k, blk, w);
-    for (int h = 0; h < 2; h++) {
+/* Isotropic unit vector, Marsaglia (1972) (reading R14): (p, q) = 2u - 1,
+ * rejected while rho = p^2 + q^2 >= 1.  The first try uses words 2 and 3 of
+ * the candidate's pair block w; further tries come two per COLL_DIR block. */
+static void marsaglia(const orc_run* R, uint32_t c, uint32_t s, uint32_t k, const uint32_t w_pair[4], float e[3]) {
+  uint32_t w[4] = {0, 0, w_pair[2], w_pair[3]};
+  int h0 = 1;                                   /* the pair block offers one try: (w2, w3) */
+  for (int32_t blk = -1; blk < 64; blk++) {
+    if (blk >= 0) { draw(R, c, s, TAG_COLL_DIR, k, (uint32_t)blk, w); h0 = 0; }
+    for (int h = h0; h < 2; h++) {
       float pp = 2.0f * u_co(w[2 * h]) - 1.0f;
       float qq = 2.0f * u_co(w[2 * h + 1]) - 1.0f;
       float rho = pp * pp + qq * qq;
@@ -504,7 +507,9 @@ static void marsaglia(const orc_run* R, uint32_t c, uint32_t s, uint32_t k, floa
 /* NTC collisions in one cell (Bird's no-time-counter scheme, cited by the
  * paper at PAPER.md:48,93; readings R12-R15 = SURVEY C-8, R13 as amended):
  *   M = floor(1/2 N (N-1) F_N/V_c (sigma g)_max dt + u)
- *   candidate k: i = lemire(a,N), j = lemire(b,N-1) (+1 if >= i);
+ *   candidate k, pair block (w0..w3): m = w0 N; i = m >> 32,
+ *   j = lemire(m mod 2^32, N-1) (+1 if >= i); u = w1; Marsaglia's first
+ *   try from (w2, w3), then COLL_DIR blocks;
  *   accept with probability sigma(g) g / (sigma g)_max, decided in fp64:
  *     HS : (u * ghat)^2 < g^2, ghat = (sigma g)_max / (pi d^2)   [no sqrt]
  *     VHS: u (sigma g)_max < sigma_c (g^2)^(1-omega)
@@ -527,22 +532,25 @@ static int64_t interact(orc_run* R, int64_t c, int32_t s, int32_t N, float* vx, 
   int64_t acc = 0;
   for (int64_t k = 0; k < M; k++) {
     draw(R, (uint32_t)c, (uint32_t)s, TAG_COLL_PAIR, (uint32_t)k, 0, w);
-    int64_t i = lemire(w[0], N);
-    int64_t j = lemire(w[1], N - 1);
+    /* the pair from word 0 alone: i = floor(w0 N / 2^32), and j from the low
+     * 32 bits of that product scaled to N - 1 (R13) */
+    const uint64_t m = (uint64_t)w[0] * (uint64_t)N;
+    int64_t i = (int64_t)(m >> 32);
+    int64_t j = lemire((uint32_t)m, N - 1);
     if (j >= i) j++;
     float dx = vx[i] - vx[j], dy = vy[i] - vy[j], dz = vz[i] - vz[j];
     float g2 = (dx * dx + dy * dy) + dz * dz;
     if (g2 > maxg2) maxg2 = g2;
     int accept;
     if (R->p.model == ORC_HS) {
-      double lhs = u_co_d(w[2]) * ghat;
+      double lhs = u_co_d(w[1]) * ghat;
       accept = lhs * lhs < (double)g2;
     } else {
-      accept = u_co_d(w[2]) * gm < sigma_g(R, g2);
+      accept = u_co_d(w[1]) * gm < sigma_g(R, g2);
     }
     if (accept) {
       float e[3];
-      marsaglia(R, (uint32_t)c, (uint32_t)s, (uint32_t)k, e);
+      marsaglia(R, (uint32_t)c, (uint32_t)s, (uint32_t)k, w, e);
       float cmx = (vx[i] + vx[j]) * 0.5f, cmy = (vy[i] + vy[j]) * 0.5f, cmz = (vz[i] + vz[j]) * 0.5f;
       float h = 0.5f * sqrtf(g2);
       vx[i] = cmx + h * e[0]; vy[i] = cmy + h * e[1]; vz[i] = cmz + h * e[2];

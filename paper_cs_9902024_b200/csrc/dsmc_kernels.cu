@@ -708,14 +708,16 @@ __global__ void __launch_bounds__(256) k_scatter(Prm P) {
 }
 
 // ============================================================= Interaction
-// Isotropic direction, Marsaglia (reading R14)
-__device__ __forceinline__ void marsaglia(uint2 key, uint32_t c, uint32_t s, uint32_t k, float e[3]) {
+// Isotropic direction, Marsaglia (reading R14): the first try from words z, w
+// of the candidate's pair block, further tries two per COLL_DIR block
+__device__ __forceinline__ void marsaglia(uint2 key, uint32_t c, uint32_t s, uint32_t k, uint4 wpair, float e[3]) {
+  uint4 w = wpair;
+  int h0 = 1;
 #pragma unroll 1
-  for (uint32_t blk = 0; blk < 64; blk++) {
-    const uint4 w = draw(key, c, s, TAG_COLL_DIR, k, blk);
+  for (int32_t blk = -1; blk < 64; blk++) {
+    if (blk >= 0) { w = draw(key, c, s, TAG_COLL_DIR, k, (uint32_t)blk); h0 = 0; }
     const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
+    for (int h = h0; h < 2; h++) {
       const float pp = 2.0f * u_co(ww[2 * h]) - 1.0f;
       const float qq = 2.0f * u_co(ww[2 * h + 1]) - 1.0f;
       const float rho = pp * pp + qq * qq;
@@ -729,6 +731,15 @@ __device__ __forceinline__ void marsaglia(uint2 key, uint32_t c, uint32_t s, uin
     }
   }
   e[0] = 0.0f; e[1] = 0.0f; e[2] = 1.0f;
+}
+
+// the candidate pair of R13 from the first word of its pair block:
+// m = w N, i = m >> 32, j = lemire(m mod 2^32, N - 1), j += (j >= i)
+__device__ __forceinline__ void pair_of(uint32_t w, uint32_t N, uint32_t& i, uint32_t& j) {
+  const uint64_t m = (uint64_t)w * N;
+  i = (uint32_t)(m >> 32);
+  j = lemire((uint32_t)m, N - 1);
+  if (j >= i) j++;
 }
 
 // velocity accessors: shared-memory tile, or global memory through LCR
@@ -776,9 +787,8 @@ __device__ __forceinline__ void collide_cell(const Prm& P, uint2 key, uint32_t c
   float maxg2 = 0.0f;
   for (uint32_t k = 0; k < (uint32_t)M; k++) {
     w = draw(key, c, s, TAG_COLL_PAIR, k, 0);
-    const uint32_t i = lemire(w.x, N);
-    uint32_t j = lemire(w.y, N - 1);
-    if (j >= i) j++;
+    uint32_t i, j;
+    pair_of(w.x, N, i, j);
     float a[3], b[3];
     acc.ld(i, a);
     acc.ld(j, b);
@@ -787,14 +797,14 @@ __device__ __forceinline__ void collide_cell(const Prm& P, uint2 key, uint32_t c
     if (g2 > maxg2) maxg2 = g2;
     bool accept;
     if (P.model == 0) {
-      const double lhs = u_co_d(w.z) * ghat;
+      const double lhs = u_co_d(w.y) * ghat;
       accept = lhs * lhs < (double)g2;
     } else {
-      accept = vhs_accept(P, w.z, gm, g2);
+      accept = vhs_accept(P, w.y, gm, g2);
     }
     if (accept) {
       float e[3];
-      marsaglia(key, c, s, k, e);
+      marsaglia(key, c, s, k, w, e);
       const float cmx = (a[0] + b[0]) * 0.5f, cmy = (a[1] + b[1]) * 0.5f, cmz = (a[2] + b[2]) * 0.5f;
       const float hh = 0.5f * sqrtf(g2);
       const float pa[3] = {cmx + hh * e[0], cmy + hh * e[1], cmz + hh * e[2]};
@@ -824,7 +834,7 @@ __device__ __forceinline__ uint32_t ntc_count(const Prm& P, uint2 key, uint32_t 
   return (uint32_t)M;
 }
 
-// Marsaglia pair from block b0 on (the first block is handled inline by k_collide)
+// Marsaglia pair from direction block b0 on (the first try, from the pair block, is made inline)
 __device__ __noinline__ void marsaglia_pq_from(uint2 key, uint32_t c, uint32_t s, uint32_t k, uint32_t b0,
                                                float& pp_out, float& qq_out) {
 #pragma unroll 1   // cold (both tries of block 0 rejected): keep the code small
@@ -842,25 +852,6 @@ __device__ __noinline__ void marsaglia_pq_from(uint2 key, uint32_t c, uint32_t s
   pp_out = 0.0f;   // never reached in practice; gives e = (0, 0, 1) like marsaglia()
   qq_out = 0.0f;
 }
-
-// the Marsaglia pair (p, q) of candidate k (reading R14), drawn ahead of use
-__device__ __forceinline__ void marsaglia_pq(uint2 key, uint32_t c, uint32_t s, uint32_t k, float& pp_out,
-                                             float& qq_out) {
-  for (uint32_t blk = 0; blk < 64; blk++) {
-    const uint4 w = draw(key, c, s, TAG_COLL_DIR, k, blk);
-    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const float pp = 2.0f * u_co(ww[2 * h]) - 1.0f;
-      const float qq = 2.0f * u_co(ww[2 * h + 1]) - 1.0f;
-      const float rho = pp * pp + qq * qq;
-      if (rho < 1.0f) { pp_out = pp; qq_out = qq; return; }
-    }
-  }
-  pp_out = 0.0f;   // never reached in practice; gives e = (0, 0, 1) like marsaglia()
-  qq_out = 0.0f;
-}
-
 
 // candidates of one cell in increasing k with everything velocity-independent
 // drawn ahead (k_collide): ij = i | j << 16; thr = HS threshold F (accept iff
@@ -1002,11 +993,11 @@ constexpr int CCW = 128;    // pre-drawn candidates per round per warp
 
 struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
   uint32_t* sorted; uint32_t* a; float* vy; float* vz; uint8_t* cell; uint8_t* mod;
-  uint32_t* cij; uint32_t* cur; float* cp; float* cq; float* ce;
+  uint32_t* cij; uint32_t* cur; float* cp; float* cq; float* ce; uint8_t* fl;
 };
 
 __host__ __device__ inline size_t warp_smem_bytes(int capw) {
-  return (size_t)capw * 18 + (size_t)CCW * 20 + 16;
+  return (size_t)capw * 18 + (size_t)CCW * 21 + 16;
 }
 
 __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
@@ -1022,6 +1013,7 @@ __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
   w.ce = w.cq + CCW;
   w.cell = reinterpret_cast<uint8_t*>(w.ce + CCW);
   w.mod = w.cell + capw;
+  w.fl = w.mod + capw;       // candidates whose first Marsaglia try was rejected
   return w;
 }
 
@@ -1033,10 +1025,13 @@ template <bool UK, int MODEL>
 __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int lane, uint32_t base, uint32_t lim,
                                             uint32_t mst, uint32_t N, double ghatu, int r, uint32_t c, uint32_t s,
                                             uint2 key_u) {
+    const unsigned lt = (1u << lane) - 1u;
+    uint32_t nfail = 0;        // candidates whose first Marsaglia try (pair block) was rejected
     for (uint32_t q0 = 0; q0 < lim; q0 += 64) {
-      uint32_t qq[2], kq[2], nc[2], cc[2];
+      uint32_t qq[2], kq[2], nc[2];
       double gq_hat[2];
       int rc[2];
+      uint32_t cc[2];
 #pragma unroll
       for (int hh = 0; hh < 2; hh++) {
         qq[hh] = q0 + 32 * hh + lane;
@@ -1054,44 +1049,70 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
         rc[hh] = __shfl_sync(FULL, r, lo);
         cc[hh] = __shfl_sync(FULL, c, lo);
       }
-      uint4 wp[2], wd[2];
+      uint4 wp[2];
 #pragma unroll
       for (int hh = 0; hh < 2; hh++) {
         const uint2 keyc = UK ? key_u : run_key(P, rc[hh]);
         wp[hh] = draw(keyc, cc[hh], s, TAG_COLL_PAIR, kq[hh], 0);
-        wd[hh] = draw(keyc, cc[hh], s, TAG_COLL_DIR, kq[hh], 0);
       }
 #pragma unroll
       for (int hh = 0; hh < 2; hh++) {
         const uint32_t q = qq[hh];
+        const float pp = 2.0f * u_co(wp[hh].z) - 1.0f, qv = 2.0f * u_co(wp[hh].w) - 1.0f;
+        const float rho = pp * pp + qv * qv;
+        const bool fail = q < lim && !(rho < 1.0f);
+        const unsigned fm = __ballot_sync(FULL, fail);
+        if (fail) W.fl[nfail + __popc(fm & lt)] = (uint8_t)q;
+        nfail += __popc(fm);
         if (q < lim) {
-          const uint32_t i = lemire(wp[hh].x, nc[hh]);
-          uint32_t j = lemire(wp[hh].y, nc[hh] - 1);
-          if (j >= i) j++;
+          uint32_t i, j;
+          pair_of(wp[hh].x, nc[hh], i, j);
           W.cij[q] = i | (j << 16);
           if (MODEL == DSMC_MODEL_HS) {
             // HS: accept iff (double)g2 > (u ghat)^2 (R13)  <=>  g2 > F, F the largest
             // float <= (u ghat)^2 -- the same decision as one fp32 compare in the walk
-            const double lhs = u_co_d(wp[hh].z) * gq_hat[hh];
+            const double lhs = u_co_d(wp[hh].y) * gq_hat[hh];
             W.cur[q] = __float_as_uint(__double2float_rd(lhs * lhs));
           } else {
-            W.cur[q] = wp[hh].z;
+            W.cur[q] = wp[hh].y;
           }
-          // Marsaglia pair: first block drawn above, further blocks only if both tries fail
-          float pp = 2.0f * u_co(wd[hh].x) - 1.0f, qv = 2.0f * u_co(wd[hh].y) - 1.0f;
-          if (!(pp * pp + qv * qv < 1.0f)) {
-            pp = 2.0f * u_co(wd[hh].z) - 1.0f;
-            qv = 2.0f * u_co(wd[hh].w) - 1.0f;
-            if (!(pp * pp + qv * qv < 1.0f))
-              marsaglia_pq_from(UK ? key_u : run_key(P, rc[hh]), cc[hh], s, kq[hh], 1, pp, qv);
+          if (!fail) {   // unit vector of R14 from the pair block's try
+            const float sr = sqrtf(1.0f - rho);
+            W.cp[q] = 2.0f * pp * sr;
+            W.cq[q] = 2.0f * qv * sr;
+            W.ce[q] = 1.0f - 2.0f * rho;
           }
-          // unit vector of R14, drawn ahead of use
-          const float rho = pp * pp + qv * qv;
-          const float sr = sqrtf(1.0f - rho);
-          W.cp[q] = 2.0f * pp * sr;
-          W.cq[q] = 2.0f * qv * sr;
-          W.ce[q] = 1.0f - 2.0f * rho;
         }
+      }
+    }
+    // rejected first tries (about one candidate in five), compacted: direction blocks
+    __syncwarp();
+    for (uint32_t f0 = 0; f0 < nfail; f0 += 32) {
+      const bool act = f0 + lane < nfail;
+      const uint32_t q = act ? W.fl[f0 + lane] : 0u;
+      const uint32_t gq = base + q;
+      int lo = 0;
+#pragma unroll
+      for (int stp = 16; stp > 0; stp >>= 1) {
+        const uint32_t m = __shfl_sync(FULL, mst, lo + stp);
+        if (m <= gq && lo + stp < 32) lo += stp;
+      }
+      const uint32_t kq = gq - __shfl_sync(FULL, mst, lo), cc = __shfl_sync(FULL, c, lo);
+      const int rc = __shfl_sync(FULL, r, lo);
+      if (act) {
+        const uint2 keyc = UK ? key_u : run_key(P, rc);
+        const uint4 wd = draw(keyc, cc, s, TAG_COLL_DIR, kq, 0);
+        float pp = 2.0f * u_co(wd.x) - 1.0f, qv = 2.0f * u_co(wd.y) - 1.0f;
+        if (!(pp * pp + qv * qv < 1.0f)) {
+          pp = 2.0f * u_co(wd.z) - 1.0f;
+          qv = 2.0f * u_co(wd.w) - 1.0f;
+          if (!(pp * pp + qv * qv < 1.0f)) marsaglia_pq_from(keyc, cc, s, kq, 1, pp, qv);
+        }
+        const float rho = pp * pp + qv * qv;
+        const float sr = sqrtf(1.0f - rho);
+        W.cp[q] = 2.0f * pp * sr;
+        W.cq[q] = 2.0f * qv * sr;
+        W.ce[q] = 1.0f - 2.0f * rho;
       }
     }
 }
@@ -1743,18 +1764,20 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
             const uint32_t nc = c_N[lo], kq = gq - c_mst[lo], o = c_st[lo] - S;
             const uint2 keyc = run_key(P, c_r[lo]);
             const uint4 w = draw(keyc, c_c[lo], (uint32_t)s, TAG_COLL_PAIR, kq, 0);
-            const uint32_t i = lemire(w.x, nc);
-            uint32_t j = lemire(w.y, nc - 1);
-            if (j >= i) j++;
+            uint32_t i, j;
+            pair_of(w.x, nc, i, j);
             s_cij[q] = (o + i) | ((o + j) << 16);
             s_clo[q] = (uint8_t)lo;
             if (P.model == 0) {
-              const double lhs = u_co_d(w.z) * c_gh[lo];
+              const double lhs = u_co_d(w.y) * c_gh[lo];
               s_cur[q] = __float_as_uint(__double2float_rd(lhs * lhs));
             } else {
-              s_cur[q] = w.z;
+              s_cur[q] = w.y;
             }
-            marsaglia_pq(keyc, c_c[lo], (uint32_t)s, kq, s_cp[q], s_cq[q]);
+            float pp = 2.0f * u_co(w.z) - 1.0f, qv = 2.0f * u_co(w.w) - 1.0f;
+            if (!(pp * pp + qv * qv < 1.0f)) marsaglia_pq_from(keyc, c_c[lo], (uint32_t)s, kq, 0, pp, qv);
+            s_cp[q] = pp;
+            s_cq[q] = qv;
           }
           __syncthreads();
           // dependency rounds: an undone candidate claims both its particles

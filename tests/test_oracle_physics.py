@@ -584,3 +584,29 @@ def test_time_average_estimators(oracle_mod):
     sd_inst = np.mean([e[:, 0].std() for e in inst])
     assert avg[:, 0].std() < 0.5 * sd_inst, (avg[:, 0].std(), sd_inst)
     assert abs(np.nanmean(avg[:, 4]) - 1.0) < 0.01      # equilibrium temperature
+
+
+def test_marsaglia_direction_isotropic(oracle_mod):
+    """R14 pin: the post-collision direction is uniform on the sphere whichever
+    try (the pair block's or a direction block's) produced it.  A two-particle
+    cell with v = (+-1, 0, 0) keeps c_m = 0 and h = 1, so after the step v_0 is
+    the last accepted candidate's unit vector e: its z must be uniform on
+    [-1, 1] (Archimedes) and its azimuth uniform on (-pi, pi]."""
+    p = configs.get("c4_small")
+    gmax = 6.0                                   # < 2 pi: every candidate of g = 2 is accepted (HS)
+    p["fnum_vc"] = 2.0 / (gmax * p["dt"])        # about two candidates per trial
+    o = oracle_mod.OracleRun(p, 0)
+    es = []
+    for t in range(6000):
+        r = o.interact_cell(t % 4096, t // 4096, np.array([1.0, -1.0]), np.zeros(2), np.zeros(2), gmax)
+        if r["acc"]:
+            assert r["acc"] == r["cand"]
+            es.append((r["vx"][0], r["vy"][0], r["vz"][0]))
+    e = np.array(es, np.float64)
+    n = len(e)
+    assert n > 4000
+    assert np.allclose(np.linalg.norm(e, axis=1), 1.0, atol=1e-6)
+    assert np.abs(e.mean(0)).max() < 4 / math.sqrt(3 * n)
+    assert stats.kstest(e[:, 2], stats.uniform(loc=-1, scale=2).cdf).pvalue > 1e-3
+    phi = np.arctan2(e[:, 1], e[:, 0])
+    assert stats.kstest(phi, stats.uniform(loc=-math.pi, scale=2 * math.pi).cdf).pvalue > 1e-3
