@@ -659,6 +659,7 @@ __global__ void k_step_end(Prm P, int mode, int slot) {
 // a chunk are issued before any result is consumed.
 __global__ void __launch_bounds__(256) k_scatter(Prm P) {
   const int lane = threadIdx.x & 31;
+  constexpr int SL = 2;      // 32-particle slices per warp iteration (returning atomics in flight)
   const unsigned lt = (1u << lane) - 1u;
   const int64_t n_items = P.ctl.items[P.R];
   __shared__ int64_t s_item;
@@ -672,33 +673,33 @@ __global__ void __launch_bounds__(256) k_scatter(Prm P) {
     // the next slice's keys are loaded before this slice's returning atomics, so
     // the HBM latency of one overlaps the L2 atomic latency of the other
     const int64_t iend = ibase + ITEM < n ? ibase + ITEM : n;
-    uint32_t kn[4];
-    int64_t i0w = ibase + (threadIdx.x >> 5) * 128;
+    uint32_t kn[SL];
+    int64_t i0w = ibase + (threadIdx.x >> 5) * (32 * SL);
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
+    for (int j = 0; j < SL; j++) {
       const int64_t i = i0w + j * 32 + lane;
       kn[j] = i < iend ? K[i] : DEAD_KEY;
     }
-    for (; i0w < iend; i0w += 1024) {
-    uint32_t kk[4], m[4], p0[4];
+    for (; i0w < iend; i0w += 256 * SL) {
+    uint32_t kk[SL], m[SL], p0[SL];
 #pragma unroll
-    for (int j = 0; j < 4; j++) kk[j] = kn[j];
-    if (i0w + 1024 < iend) {
+    for (int j = 0; j < SL; j++) kk[j] = kn[j];
+    if (i0w + 256 * SL < iend) {
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const int64_t i = i0w + 1024 + j * 32 + lane;
+      for (int j = 0; j < SL; j++) {
+        const int64_t i = i0w + 256 * SL + j * 32 + lane;
         kn[j] = i < iend ? K[i] : DEAD_KEY;
       }
     }
 #pragma unroll
-    for (int j = 0; j < 4; j++) m[j] = __match_any_sync(FULL, kk[j]);
+    for (int j = 0; j < SL; j++) m[j] = __match_any_sync(FULL, kk[j]);
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
+    for (int j = 0; j < SL; j++) {
       p0[j] = 0;
       if (kk[j] != DEAD_KEY && lane == __ffs(m[j]) - 1) p0[j] = atomicAdd(&P.cell[kk[j]], (uint32_t)__popc(m[j]));
     }
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
+    for (int j = 0; j < SL; j++) {
       const uint32_t b = __shfl_sync(FULL, p0[j], __ffs(m[j]) - 1);
       if (kk[j] != DEAD_KEY) P.lcr[b + __popc(m[j] & lt)] = (uint32_t)(base + i0w + j * 32 + lane);
     }
