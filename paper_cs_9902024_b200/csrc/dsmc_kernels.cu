@@ -464,7 +464,7 @@ __device__ __forceinline__ bool move_one(const Prm& P, uint2 key, uint32_t idx, 
 // / LCR segments they hit stay resident in L2.  The last block to finish
 // resets the cursor for the next launch.
 constexpr int ITEM_M = 8192;   // Motion's work item (measured at c4: 4096 / 8192 / 16384: 4.50 / 4.38 / 4.40 ms)
-constexpr int ITEM_S = 4096;   // the scatter's (8192 made it 2.32 -> 2.40 ms)
+constexpr int ITEM_S = 4096;   // the scatter's (2048 / 4096 / 8192: 2.42 / 2.32 / 2.40 ms)
 __device__ __forceinline__ int64_t queue_next(unsigned long long* q, int64_t* s_item) {
   __syncthreads();
   if (threadIdx.x == 0) *s_item = (int64_t)atomicAdd(q, 1ull);
