@@ -238,7 +238,20 @@ void orc_destroy(orc_run* R) {
   free(R);
 }
 
-static void latch(orc_run* R, int32_t code) { if (R->status == 0) R->status = code; }
+/* Fault latch (reading R24): keep the most severe fault seen so far,
+ * ENONFINITE > EINDEX > ECELL > EBOUNCE > ECAP, so the reported code does not
+ * depend on the order in which particles or cells are visited. */
+static int fault_rank(int32_t code) {
+  switch (code) {
+    case ORC_ENONFINITE: return 5;
+    case ORC_EINDEX: return 4;
+    case ORC_ECELL: return 3;
+    case ORC_EBOUNCE: return 2;
+    case ORC_ECAP: return 1;
+    default: return 0;
+  }
+}
+static void latch(orc_run* R, int32_t code) { if (fault_rank(code) > fault_rank(R->status)) R->status = code; }
 
 /* --------------------------------------------------------- Generation -- */
 /* Initial fill (SURVEY C-3): cells in increasing flat index,
@@ -525,7 +538,7 @@ static int64_t interact(orc_run* R, int64_t c, int32_t s, int32_t N, float* vx, 
   uint32_t w[4];
   draw(R, (uint32_t)c, (uint32_t)s, TAG_COLL_COUNT, 0, 0, w);
   int64_t M = (int64_t)floor(x + u_co_d(w[0]));
-  if (M > 0xFFFFFF) { latch(R, ORC_EPARAM); M = 0xFFFFFF; }
+  if (M > 0xFFFFFF) { latch(R, ORC_ECELL); M = 0xFFFFFF; }
   *n_cand = M;
   const double ghat = gm / R->sigma_c;
   float maxg2 = 0.0f;

@@ -28,7 +28,10 @@ enum { ORC_HS = 0, ORC_VHS = 1 };
 enum { ORC_INFLOW_NONE = 0, ORC_INFLOW_GHOST = 1, ORC_INFLOW_EFFUSIVE = 2 };
 /* error / fault codes (same meaning as the product ABI, defined independently) */
 enum { ORC_OK = 0, ORC_EINVAL = -1, ORC_ECLOCK = -2, ORC_EPARAM = -3, ORC_ECAP = -4,
-       ORC_EINDEX = -5, ORC_ENONFINITE = -6, ORC_ESCHED = -8, ORC_EBOUNCE = -9 };
+       ORC_EINDEX = -5, ORC_ENONFINITE = -6, ORC_ESCHED = -8, ORC_EBOUNCE = -9, ORC_ECELL = -10 };
+/* Run-time faults are latched by precedence, not by arrival (DESIGN.md reading
+ * R24): the latched code is the most severe one seen so far, in the order
+ * ENONFINITE > EINDEX > ECELL > EBOUNCE > ECAP. */
 
 typedef struct {
   int32_t lo[3], hi[3];  /* cell box [lo, hi) per axis */

@@ -14,6 +14,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
+# mutation testing (tools/mutate_oracle.py) points this at a mutant build
+LIB_OVERRIDE = os.environ.get("DSMC_ORACLE_LIB")
 SRC = os.path.join(HERE, "dsmc_oracle.c")
 CFLAGS = ["-O2", "-std=gnu11", "-Wall", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
 
@@ -79,8 +81,11 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = C.CDLL(LIB_PATH)
+        if LIB_OVERRIDE:
+            L = C.CDLL(LIB_OVERRIDE)
+        else:
+            build()
+            L = C.CDLL(LIB_PATH)
         P = C.POINTER
         vp = C.c_void_p
         L.orc_create.restype = vp

@@ -73,6 +73,8 @@ int validate(const dsmc_problem* p) {
   if (p->dim < 1 || p->dim > 3 || p->nx < 1 || p->ny < 1 || p->nz < 1) return fail(DSMC_EINVAL, "bad grid");
   if ((p->dim < 2 && p->ny != 1) || (p->dim < 3 && p->nz != 1)) return fail(DSMC_EINVAL, "unused axes must have 1 cell");
   if (p->n_runs < 1 || p->cap_per_run < 1 || p->n_fill < 0 || p->n_fill > 4) return fail(DSMC_EINVAL, "bad batch/fill");
+  // the run index is gridDim.y of the fill and inflow kernels
+  if (p->n_runs > 65535) return fail(DSMC_EINVAL, "n_runs > 65535 (grid y limit of the generation kernels)");
   if (!(p->dt > 0) || !(p->dt_s >= p->dt) || !(p->dt_L >= p->dt_s)) return fail(DSMC_ECLOCK, "need 0 < dt <= dt_s <= dt_L");
   const double ks = p->dt_s / p->dt, kl = p->dt_L / p->dt_s;
   if (std::fabs(ks - std::floor(ks + 0.5)) > 1e-9 * ks || std::fabs(kl - std::floor(kl + 0.5)) > 1e-9 * kl)
@@ -499,8 +501,10 @@ int dsmc_slot_samples(dsmc_ctx* c, int32_t slot, int32_t* out) {
 }
 
 static int latched(dsmc_ctx* c, int32_t* st) {
-  CK(cudaMemcpyAsync(st, c->P.ctl.status, 4, cudaMemcpyDeviceToHost, c->stream));
+  uint32_t w = 0;
+  CK(cudaMemcpyAsync(&w, c->P.ctl.status, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  *st = dsmc::status_code(w);
   return DSMC_OK;
 }
 
@@ -548,14 +552,16 @@ int dsmc_status(dsmc_ctx* c, int64_t* counters_out) {
   std::vector<unsigned long long> cnt(4 * (size_t)R);
   std::vector<int64_t> ns((size_t)R), live((size_t)R);
   std::vector<unsigned long long> ps((size_t)R);
-  int32_t step = 0, st = 0;
+  int32_t step = 0;
+  uint32_t stw = 0;
   CK(cudaMemcpyAsync(cnt.data(), c->P.ctl.counters, 8 * 4 * (size_t)R, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(ns.data(), c->P.ctl.n_store, 8 * (size_t)R, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(live.data(), c->P.ctl.live, 8 * (size_t)R, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(ps.data(), c->P.ctl.psteps, 8 * (size_t)R, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(&step, c->P.ctl.step, 4, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(&st, c->P.ctl.status, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&stw, c->P.ctl.status, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  const int32_t st = dsmc::status_code(stw);
   if (counters_out)
     for (int r = 0; r < R; r++) {
       for (int q = 0; q < 4; q++) counters_out[r * 8 + q] = (int64_t)cnt[r * 4 + q];

@@ -152,7 +152,19 @@ __device__ __forceinline__ float place(int32_t i, uint32_t w) {
 
 __device__ __forceinline__ int32_t axis_n(const Prm& P, int a) { return a == 0 ? P.nx : (a == 1 ? P.ny : P.nz); }
 
-__device__ __forceinline__ void latch(const Prm& P, int32_t code) { atomicCAS(P.ctl.status, 0, code); }
+// Fault latch (reading R24): the control word keeps the most severe fault seen,
+// ENONFINITE > EINDEX > ECELL > EBOUNCE > ECAP, whatever the order in which
+// threads report them -- atomicMax over rank << 8 | -code; the host decodes it
+// with status_code().
+__host__ __device__ __forceinline__ uint32_t fault_word(int32_t code) {
+  const uint32_t rank = code == ST_NONFINITE ? 5u : code == ST_INDEX ? 4u : code == ST_CELL ? 3u
+                      : code == ST_BOUNCE ? 2u : code == ST_CAP ? 1u : 0u;
+  return rank ? (rank << 8) | (uint32_t)(-code) : 0u;
+}
+__host__ __device__ __forceinline__ int32_t status_code(uint32_t word) { return -(int32_t)(word & 0xFFu); }
+__device__ __forceinline__ void latch(const Prm& P, int32_t code) {
+  atomicMax(reinterpret_cast<unsigned int*>(P.ctl.status), fault_word(code));
+}
 
 // P array a (0..5 = x,y,z,vx,vy,vz) of half h
 __device__ __forceinline__ float* parr(const Prm& P, int h, int a) {

@@ -552,3 +552,25 @@ def test_staging_capacity_does_not_change_results(dsmc_gpu, monkeypatch, name, s
             sa, sb = sim.get_state(r), ref.get_state(r)
             for k in sa:
                 assert np.array_equal(sa[k], sb[k]), (capw, r, k)
+
+
+@pytest.mark.parametrize("nan_pos", [3, 4000, None])
+def test_fault_code_parity(dsmc_gpu, oracle_mod, nan_pos):
+    """Reading R24: the same fault precedence on both sides.  A NaN velocity (before
+    or after an out-of-domain particle in store order) latches ENONFINITE (-6) on the
+    GPU and in the oracle; the out-of-domain particle alone latches EINDEX (-5)."""
+    p = configs.get("c4_small", n_runs=1)
+    st = inputs.random_state(3, p, 4096)
+    st["x"][7] = np.float32(3 * p["nx"] + 0.5)
+    st["vx"][7] = np.float32(0.0)
+    if nan_pos is not None:
+        st["vx"][nan_pos] = np.float32("nan")
+    ref = oracle_mod.OracleRun(p, 0)
+    ref.set_state(st)
+    ref.step(1)
+    sim = dsmc_gpu.Simulation(p)
+    sim.generate()
+    sim.set_state(0, st, step=0)
+    sim.step(1)
+    rc, _ = sim.status(raise_on_fault=False)
+    assert rc == ref.status == (-6 if nan_pos is not None else -5), (rc, ref.status)
