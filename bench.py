@@ -30,6 +30,21 @@ sys.path.insert(0, ROOT)
 from workloads import configs  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# arithmetic types of the path (R6): fp32 particle state and majorant,
+# fp64 candidate count, acceptance test and sampled sums
+DTYPE = "f32 (state, majorant) + f64 (NTC count, acceptance, sums)"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical CPUs)"
+    except OSError:
+        pass
+    return None
+
+
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
 
@@ -263,14 +278,17 @@ def run_ours(args):
         _, sa = sim.status()
         sim.step(K)
         sim.sample(0)
-        macros = sim.read_macros(0)
+        # the paper's one exchange: every rank's slot sums gathered
+        # in run order (NCCL all-gather; one block on one GPU), then the ensemble
+        macros = runs.ensemble_over_ranks(sim, 0)
         t1 = time.perf_counter()
         _, sb = sim.status()
         ps_e2e = sum(b["particle_steps"] - a["particle_steps"] for a, b in zip(sa, sb))
         e2e_val = runs.sum_over_ranks(ps_e2e) / runs.max_over_ranks(t1 - t0)
         e2e = {"value": e2e_val, "unit": "particle-steps/s", "h2d_bytes_per_step": nbytes_h2d // K,
                "d2h_bytes_per_step": macros.nbytes // K,
-               "what": "set_state(all runs, pinned host) + K graph steps + dsmc_sample + dsmc_read_macros"}
+               "what": "set_state(all runs, pinned host) + K graph steps + dsmc_sample + gather of the slot "
+                       "sums over ranks + dsmc_read_macros_gathered (macros to host)"}
 
     rc, _ = sim.status(raise_on_fault=False)
     cpu = None
@@ -281,7 +299,7 @@ def run_ours(args):
             "metric": "particle-steps/sec per B200 (all runs batched); % of HBM roofline",
             "value": value, "unit": "particle-steps/s", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32 state / f64 per-cell", "data": "synthetic",
+            "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
             "config": {"workload": f"{args.config}: " + configs.PRESETS[args.config].__doc__.split("\n")[0],
                        "n_runs_per_gpu": p["n_runs"], "cells_per_run": configs.n_cells(p),
                        "particles_per_step": live_avg, "reorder_every": p["reorder_every"],
@@ -322,7 +340,7 @@ def cpu_baseline(p, budget_s=12.0):
         if time.perf_counter() - t0 > budget_s or steps >= configs.n_steps(p):
             break
     el = time.perf_counter() - t0
-    return {"value": ps / el, "unit": "particle-steps/s", "cores": 1, "kind": "oracle",
+    return {"value": ps / el, "unit": "particle-steps/s", "cores": 1, "kind": "oracle", "cpu": cpu_model(),
             "sample": f"run {p['run_id0']} of the same workload, steps 0..{steps - 1} ({ps} particle-steps, {el:.1f} s)"}
 
 
@@ -346,9 +364,9 @@ def run_reference(args):
         "impl": "reference", "metric": "particle-steps/sec per B200 (all runs batched); % of HBM roofline",
         "value": v, "unit": "particle-steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32 state / f64 per-cell", "data": "synthetic",
+        "dtype": DTYPE, "data": "synthetic",
         "config": {"workload": f"{args.config} (oracle sample: run 0 of the batch)"},
-        "cpu_baseline": {"value": v, "unit": "particle-steps/s", "cores": 1, "kind": "oracle",
+        "cpu_baseline": {"value": v, "unit": "particle-steps/s", "cores": 1, "kind": "oracle", "cpu": cpu_model(),
                          "sample": f"run 0 only, steps {args.warmup}..{args.warmup + args.steps - 1}"},
         "e2e": {"value": v, "unit": "particle-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))

@@ -8,7 +8,7 @@
  * runs at once (the outer loop (2), becomes a batch axis).
  * The random number generator is "shifted" per run (PAPER.md:113-115,
  * 435-437) by keying a counter-based Philox4x32-10 with (seed, run id).
- * The exact semantics of every step are DESIGN.md readings R1-R23.
+ * The exact semantics of every step are DESIGN.md readings R1-R24.
  *
  * Conventions for every entry point:
  *   - Return value: DSMC_OK (0) or a negative dsmc_rc code.  No C++
@@ -16,12 +16,16 @@
  *     last failure on the calling thread is dsmc_last_error().
  *   - Device buffers are allocated and owned by the CALLER (the Python binding
  *     uses torch), sized by dsmc_query_sizes(); the library borrows them from
- *     dsmc_create() until dsmc_destroy() and never calls cudaMalloc.  It owns
- *     only its CUDA graph and a small pinned staging area.
+ *     dsmc_create() until dsmc_destroy() and allocates no device memory on the
+ *     DSMC path.  A context owns its CUDA graph (and graph exec) and a capture
+ *     stream, released by dsmc_destroy.  The one exception is the test hook
+ *     dsmc_selftest_philox, which allocates and frees its own scratch buffers.
  *   - All calls are asynchronous on the caller's CUDA stream except those
  *     marked SYNC, which synchronise that stream.  Device-side faults
- *     (capacity, indexing, non-finite velocity, bounce limit) are latched in
- *     the control block and returned by the next SYNC call.
+ *     (capacity, indexing, non-finite velocity, bounce limit, cell size) are
+ *     latched in the control block and returned by the next SYNC call; when
+ *     several occur the most severe is kept, ENONFINITE > EINDEX > ECELL >
+ *     EBOUNCE > ECAP (reading R24), so the code does not depend on thread order.
  *   - Store order: run r owns particle slots [r*stride, r*stride + cap) of each
  *     SoA array (x, y, z, vx, vy, vz); "store index" i of run r is the offset
  *     inside that window.  Host arrays passed to the test/checkpoint hooks are
@@ -154,6 +158,31 @@ int dsmc_read_macros(dsmc_ctx* ctx, int32_t slot, double* out);
 
 /* SYNC. Raw per-run sums of one slot -> host out[5][n_runs*Nc] (fp64). */
 int dsmc_read_sums(dsmc_ctx* ctx, int32_t slot, double* out);
+
+/* The paper's single exchange across processors ("the data
+ * exchange between processors goes after all calculation are finished. Only one
+ * processor sequentially analyzes the results"), for a job whose runs are
+ * sharded over several contexts (one per GPU).
+ *
+ * dsmc_slot_sums_ptr: DEVICE pointer (borrowed, valid until dsmc_destroy; the
+ * caller-owned C buffer) to slot `slot`'s sums, [5][n_runs*Nc] fp64 -- the
+ * send buffer of a collective (an all-gather over NVLink) without a host copy.
+ * Asynchronous-safe: no stream work.  DSMC_ESCHED for a slot out of range.
+ *
+ * dsmc_read_macros_gathered: SYNC.  Ensemble analysis of one slot over
+ * n_blocks * n_runs runs.  sums_dev: DEVICE array [n_blocks][5][n_runs*Nc]
+ * fp64; block b holds the slot sums of the context with runs
+ * [b*n_runs, (b+1)*n_runs) of the job (every context built with the same
+ * problem, n_runs and schedule; the blocks in ascending run id, i.e. rank
+ * order).  The fold over runs is in ascending global run id, exactly as
+ * dsmc_read_macros folds one context's runs, so the result is bit-identical to
+ * one context holding all the runs.  Samples per run (m, R23) are this
+ * context's for the slot.  out: host [Nc][10] as dsmc_read_macros.  Borrowed
+ * sums_dev is only read, on this context's stream; DSMC_EINVAL if it is not
+ * device memory or n_blocks < 1; DSMC_ESCHED if the slot is unwritten here. */
+int dsmc_slot_sums_ptr(dsmc_ctx* ctx, int32_t slot, const double** out);
+int dsmc_read_macros_gathered(dsmc_ctx* ctx, int32_t slot, const double* sums_dev, int32_t n_blocks,
+                              double* out);
 
 /* SYNC. Returns the latched device fault (or OK); counters_out (may be NULL)
  * receives per run {inserted, removed, candidates, accepted, n_store, step,

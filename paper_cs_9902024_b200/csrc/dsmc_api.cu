@@ -359,7 +359,13 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   P.caph_tier[0] = 3584;      // 2 blocks per SM within the 196 KB carveout (4096: 215 KB, L1 down to 28 KB, 2-3% slower; a third tier of 1024, register-limited to 2 blocks too, measured slower)
   P.caph_tier[1] = P.caph;    // 1 block per SM
 
-  auto bail = [&](int code) { delete c; return code; };
+  auto bail = [&](int code) {   // release whatever was created before the failure
+    if (c->exec) cudaGraphExecDestroy(c->exec);
+    if (c->graph) cudaGraphDestroy(c->graph);
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+    delete c;
+    return code;
+  };
   std::vector<int32_t> fj, fk;
   std::vector<uint8_t> open;
   face_lists(p, fj, fk, open);
@@ -383,8 +389,14 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   if ((e = cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
     return bail(cuda_fail(e, "cudaStreamBeginCapture"));
   dsmc::issue_step(P, c->cap_stream, dsmc::LaunchHook{});
-  if ((e = cudaStreamEndCapture(c->cap_stream, &c->graph)) != cudaSuccess) return bail(cuda_fail(e, "cudaStreamEndCapture"));
-  if ((e = cudaGraphInstantiate(&c->exec, c->graph, 0)) != cudaSuccess) return bail(cuda_fail(e, "cudaGraphInstantiate"));
+  if ((e = cudaStreamEndCapture(c->cap_stream, &c->graph)) != cudaSuccess) {
+    c->graph = nullptr;
+    return bail(cuda_fail(e, "cudaStreamEndCapture"));
+  }
+  if ((e = cudaGraphInstantiate(&c->exec, c->graph, 0)) != cudaSuccess) {
+    c->exec = nullptr;
+    return bail(cuda_fail(e, "cudaGraphInstantiate"));
+  }
   size_t nn = 0;
   cudaGraphGetNodes(c->graph, nullptr, &nn);
   std::vector<cudaGraphNode_t> nodes(nn);
@@ -438,8 +450,20 @@ int dsmc_step_timed(dsmc_ctx* c, int32_t nsteps, double* ms_accum, int64_t* laun
   if (!c || !ms_accum) return fail(DSMC_EINVAL, "bad argument");
   TimedHook h;
   h.st = c->stream;
+  std::memset(h.ev, 0, sizeof(h.ev));
+  auto destroy_events = [&]() {
+    for (int k = 0; k < dsmc::KSLOT_COUNT; k++)
+      for (int a = 0; a < 2; a++) if (h.ev[k][a]) cudaEventDestroy(h.ev[k][a]);
+  };
   for (int k = 0; k < dsmc::KSLOT_COUNT; k++)
-    for (int a = 0; a < 2; a++) CK(cudaEventCreate(&h.ev[k][a]));
+    for (int a = 0; a < 2; a++) {
+      const cudaError_t e = cudaEventCreate(&h.ev[k][a]);
+      if (e != cudaSuccess) {
+        h.ev[k][a] = nullptr;
+        destroy_events();
+        return cuda_fail(e, "cudaEventCreate");
+      }
+    }
   dsmc::LaunchHook hook;
   hook.fn = &TimedHook::cb;
   hook.user = &h;
@@ -457,8 +481,7 @@ int dsmc_step_timed(dsmc_ctx* c, int32_t nsteps, double* ms_accum, int64_t* laun
       if (launches) launches[k] += 1;
     }
   }
-  for (int k = 0; k < dsmc::KSLOT_COUNT; k++)
-    for (int a = 0; a < 2; a++) cudaEventDestroy(h.ev[k][a]);
+  destroy_events();
   return rc;
 }
 
@@ -516,6 +539,21 @@ static int slot_written(dsmc_ctx* c, int32_t slot, bool* ok) {
   return DSMC_OK;
 }
 
+// ensemble of n_blocks blocks of slot sums (block 0 may be this context's own slot) -> host out
+static int macros_from(dsmc_ctx* c, int32_t slot, const double* sums, int32_t n_blocks, double* out) {
+  int32_t m = 0;
+  CK(cudaMemcpyAsync(&m, c->P.ctl.slot_done + slot, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  dsmc::launch_macros(c->P, sums, n_blocks, m, c->prob.fnum_vc, c->stream);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, c->P.macros, 8 * 10 * (size_t)c->L.Nc, cudaMemcpyDeviceToHost, c->stream));
+  int32_t st = 0;
+  const int rc = latched(c, &st);
+  if (rc) return rc;
+  if (st) return fail(st, "latched device fault");
+  return DSMC_OK;
+}
+
 int dsmc_read_macros(dsmc_ctx* c, int32_t slot, double* out) {
   if (!c || !out) return fail(DSMC_EINVAL, "bad argument");
   if (slot < 0 || slot >= c->L.sz.n_slots) return fail(DSMC_ESCHED, "slot out of range");
@@ -523,13 +561,29 @@ int dsmc_read_macros(dsmc_ctx* c, int32_t slot, double* out) {
   int rc = slot_written(c, slot, &ok);
   if (rc) return rc;
   if (!ok) return fail(DSMC_ESCHED, "slot not written yet");
-  dsmc::launch_macros(c->P, slot, c->prob.fnum_vc, c->stream);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(out, c->P.macros, 8 * 10 * (size_t)c->L.Nc, cudaMemcpyDeviceToHost, c->stream));
-  int32_t st = 0;
-  rc = latched(c, &st);
+  return macros_from(c, slot, c->P.C + (size_t)slot * 5 * (size_t)c->L.RN, 1, out);
+}
+
+int dsmc_read_macros_gathered(dsmc_ctx* c, int32_t slot, const double* sums_dev, int32_t n_blocks, double* out) {
+  if (!c || !out || !sums_dev || n_blocks < 1) return fail(DSMC_EINVAL, "bad argument");
+  if (slot < 0 || slot >= c->L.sz.n_slots) return fail(DSMC_ESCHED, "slot out of range");
+  if ((int64_t)n_blocks * c->prob.n_runs > 0x7FFFFFFF) return fail(DSMC_EINVAL, "too many runs");
+  bool ok = false;
+  int rc = slot_written(c, slot, &ok);
   if (rc) return rc;
-  if (st) return fail(st, "latched device fault");
+  if (!ok) return fail(DSMC_ESCHED, "slot not written yet");
+  cudaPointerAttributes pa;
+  if (cudaPointerGetAttributes(&pa, sums_dev) != cudaSuccess || pa.type != cudaMemoryTypeDevice) {
+    cudaGetLastError();
+    return fail(DSMC_EINVAL, "sums_dev is not device memory");
+  }
+  return macros_from(c, slot, sums_dev, n_blocks, out);
+}
+
+int dsmc_slot_sums_ptr(dsmc_ctx* c, int32_t slot, const double** out) {
+  if (!c || !out) return fail(DSMC_EINVAL, "bad argument");
+  if (slot < 0 || slot >= c->L.sz.n_slots) return fail(DSMC_ESCHED, "slot out of range");
+  *out = c->P.C + (size_t)slot * 5 * (size_t)c->L.RN;
   return DSMC_OK;
 }
 
@@ -694,18 +748,23 @@ int dsmc_selftest_philox(int64_t n, const uint32_t* ctr, uint32_t k0, uint32_t k
   if (n <= 0 || !ctr || !out) return fail(DSMC_EINVAL, "bad argument");
   uint32_t *d_ctr = nullptr, *d_out = nullptr, *d_ref = nullptr;
   const size_t b = 16 * (size_t)n;
-  CK(cudaMalloc(&d_ctr, b));
-  CK(cudaMalloc(&d_out, b));
-  if (out_ref) CK(cudaMalloc(&d_ref, b));
-  CK(cudaMemcpy(d_ctr, ctr, b, cudaMemcpyHostToDevice));
-  dsmc::launch_selftest_philox(n, d_ctr, k0, k1, d_out, d_ref, 0);
-  CK(cudaGetLastError());
-  CK(cudaMemcpy(out, d_out, b, cudaMemcpyDeviceToHost));
-  if (out_ref) CK(cudaMemcpy(out_ref, d_ref, b, cudaMemcpyDeviceToHost));
-  cudaFree(d_ctr);
-  cudaFree(d_out);
+  int rc = DSMC_OK;
+  cudaError_t e = cudaSuccess;
+  // test hook: the only entry point that allocates device memory (freed on every exit path)
+  if ((e = cudaMalloc(&d_ctr, b)) != cudaSuccess || (e = cudaMalloc(&d_out, b)) != cudaSuccess ||
+      (out_ref && (e = cudaMalloc(&d_ref, b)) != cudaSuccess) ||
+      (e = cudaMemcpy(d_ctr, ctr, b, cudaMemcpyHostToDevice)) != cudaSuccess) {
+    rc = cuda_fail(e, "selftest setup");
+  } else {
+    dsmc::launch_selftest_philox(n, d_ctr, k0, k1, d_out, d_ref, 0);
+    if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaMemcpy(out, d_out, b, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+        (out_ref && (e = cudaMemcpy(out_ref, d_ref, b, cudaMemcpyDeviceToHost)) != cudaSuccess))
+      rc = cuda_fail(e, "selftest");
+  }
+  if (d_ctr) cudaFree(d_ctr);
+  if (d_out) cudaFree(d_out);
   if (d_ref) cudaFree(d_ref);
-  return DSMC_OK;
+  return rc;
 }
 
 }  // extern "C"

@@ -1923,39 +1923,45 @@ __device__ __forceinline__ void moments(double sn, double sx, double sy, double 
   }
 }
 
-__global__ void k_macros(Prm P, int slot, double fnum_vc) {
+// S: n_blocks blocks of [5][R*Nc] (block b = the slot sums of the context holding
+// runs b*R .. b*R + R - 1 of the job, e.g. gathered from every rank); the fold over
+// runs is in ascending global run id, so one block is the single-context case
+__global__ void k_macros(Prm P, const double* __restrict__ S, int n_blocks, int m_i, double fnum_vc) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= P.Nc) return;
   const int64_t RN = (int64_t)P.R * P.Nc;
-  const double* C = P.C + (int64_t)slot * 5 * RN;
+  const int nr = n_blocks * P.R;
+  auto at = [&](int q, int r) {   // sums of quantity q, global run r
+    const int b = r / P.R, rl = r - b * P.R;
+    return S[((int64_t)b * 5 + q) * RN + (int64_t)rl * P.Nc + c];
+  };
   double tot[5] = {0, 0, 0, 0, 0};
-  for (int r = 0; r < P.R; r++)
-    for (int q = 0; q < 5; q++) tot[q] += C[q * RN + (int64_t)r * P.Nc + c];
+  for (int r = 0; r < nr; r++)
+    for (int q = 0; q < 5; q++) tot[q] += at(q, r);
   // samples per run in the slot: 1 for a snapshot, m for a time average
-  const int32_t m_i = P.ctl.slot_done[slot];
   const double m = m_i > 0 ? (double)m_i : 1.0;
   double full[5];
-  moments(tot[0], tot[1], tot[2], tot[3], tot[4], fnum_vc, (double)P.R * m, full);
+  moments(tot[0], tot[1], tot[2], tot[3], tot[4], fnum_vc, (double)nr * m, full);
   double* o = P.macros + c * 10;
   for (int q = 0; q < 5; q++) o[q] = full[q];
-  if (P.R < 2) { for (int q = 0; q < 5; q++) o[5 + q] = 0.0; return; }
+  if (nr < 2) { for (int q = 0; q < 5; q++) o[5 + q] = 0.0; return; }
   // two passes over runs: mean of leave-one-out estimates, then spread
   double mean[5] = {0, 0, 0, 0, 0};
-  for (int r = 0; r < P.R; r++) {
+  for (int r = 0; r < nr; r++) {
     double part[5], loo[5];
-    for (int q = 0; q < 5; q++) part[q] = tot[q] - C[q * RN + (int64_t)r * P.Nc + c];
-    moments(part[0], part[1], part[2], part[3], part[4], fnum_vc, (double)(P.R - 1) * m, loo);
+    for (int q = 0; q < 5; q++) part[q] = tot[q] - at(q, r);
+    moments(part[0], part[1], part[2], part[3], part[4], fnum_vc, (double)(nr - 1) * m, loo);
     for (int q = 0; q < 5; q++) mean[q] += loo[q];
   }
-  for (int q = 0; q < 5; q++) mean[q] /= (double)P.R;
+  for (int q = 0; q < 5; q++) mean[q] /= (double)nr;
   double ss[5] = {0, 0, 0, 0, 0};
-  for (int r = 0; r < P.R; r++) {
+  for (int r = 0; r < nr; r++) {
     double part[5], loo[5];
-    for (int q = 0; q < 5; q++) part[q] = tot[q] - C[q * RN + (int64_t)r * P.Nc + c];
-    moments(part[0], part[1], part[2], part[3], part[4], fnum_vc, (double)(P.R - 1) * m, loo);
+    for (int q = 0; q < 5; q++) part[q] = tot[q] - at(q, r);
+    moments(part[0], part[1], part[2], part[3], part[4], fnum_vc, (double)(nr - 1) * m, loo);
     for (int q = 0; q < 5; q++) { const double d = loo[q] - mean[q]; ss[q] += d * d; }
   }
-  for (int q = 0; q < 5; q++) o[5 + q] = sqrt((double)(P.R - 1) / (double)P.R * ss[q]);
+  for (int q = 0; q < 5; q++) o[5 + q] = sqrt((double)(nr - 1) / (double)nr * ss[q]);
 }
 
 __global__ void k_selftest_philox(int64_t n, const uint32_t* ctr, uint2 key, uint32_t* out, uint32_t* out_ref) {
@@ -1971,15 +1977,22 @@ __global__ void k_selftest_philox(int64_t n, const uint32_t* ctr, uint2 key, uin
 }
 
 // ============================================================ host launchers
-static int g_num_sms = 0;
+// per-device launch caches (function attributes and occupancy are per device):
+// indexed by the current device ordinal
+constexpr int MAX_DEV = 64;
+static int cur_dev() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d >= 0 && d < MAX_DEV ? d : 0;
+}
+static int g_num_sms[MAX_DEV] = {0};
 static int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  const int dev = cur_dev();
+  if (!g_num_sms[dev]) {
+    cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms[dev] <= 0) g_num_sms[dev] = 148;
   }
-  return g_num_sms;
+  return g_num_sms[dev];
 }
 
 static unsigned grid_cap(int64_t work, int threads, int64_t max_blocks) {
@@ -2023,7 +2036,8 @@ void launch_fill(const Prm& P, cudaStream_t st) {
 
 template <int D, bool EV>
 static void motion_t(const Prm& P, int mode, cudaStream_t st) {
-  static int occ = 0;
+  static int occ_dev[MAX_DEV] = {0};
+  int& occ = occ_dev[cur_dev()];
   if (!occ) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_motion<D, EV>, 256, 0);
     if (occ < 1) occ = 1;
@@ -2054,7 +2068,8 @@ void launch_items(const Prm& P, cudaStream_t st, bool motion) {
 }
 
 void launch_scatter(const Prm& P, cudaStream_t st) {
-  static int occ = 0;
+  static int occ_dev[MAX_DEV] = {0};
+  int& occ = occ_dev[cur_dev()];
   if (!occ) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter, 256, 0);
     if (occ < 1) occ = 1;
@@ -2086,7 +2101,8 @@ static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t s
   const int64_t warps = (RN + 31) / 32;
   const unsigned g = (unsigned)((warps + WPB - 1) / WPB);
   const size_t smem = WPB * warp_smem_bytes(capw);
-  static size_t configured = 0;
+  static size_t configured_dev[MAX_DEV] = {0};
+  size_t& configured = configured_dev[cur_dev()];
   if (smem > configured) {
     cudaFuncSetAttribute(k_collide<D, NET, MODEL, STEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (const char* e = getenv("DSMC_CARVEOUT"))   // A/B experiments: shared-memory carveout (percent)
@@ -2122,8 +2138,11 @@ void launch_collide(const Prm& P, int mode, int slot, cudaStream_t st) {
 template <int D, int HT>
 static void heavy_t(const Prm& P, int mode, int slot, int caph, int queue, cudaStream_t st) {
   const size_t smem = heavy_smem_bytes(caph);
-  static bool configured = false;
-  static int occ = 0;
+  static bool configured_dev[MAX_DEV] = {false};
+  static int occ_dev[MAX_DEV] = {0};
+  const int dev = cur_dev();
+  bool& configured = configured_dev[dev];
+  int& occ = occ_dev[dev];
   if (!configured) {
     cudaFuncSetAttribute(k_collide_heavy<D, HT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)heavy_smem_bytes(8192));
     configured = true;
@@ -2158,8 +2177,8 @@ void launch_step_end(const Prm& P, int mode, int slot, cudaStream_t st) {
   k_step_end<<<(P.R + 127) / 128, 128, 0, st>>>(P, mode, slot);
 }
 
-void launch_macros(const Prm& P, int slot, double fnum_vc, cudaStream_t st) {
-  k_macros<<<(unsigned)((P.Nc + 127) / 128), 128, 0, st>>>(P, slot, fnum_vc);
+void launch_macros(const Prm& P, const double* sums, int n_blocks, int m, double fnum_vc, cudaStream_t st) {
+  k_macros<<<(unsigned)((P.Nc + 127) / 128), 128, 0, st>>>(P, sums, n_blocks, m, fnum_vc);
 }
 
 void launch_selftest_philox(int64_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out,

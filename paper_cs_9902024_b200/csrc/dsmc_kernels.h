@@ -36,7 +36,7 @@ void launch_zero(uint32_t* a, int64_t n, cudaStream_t st);
 void launch_fill_f32(float* a, int64_t n, float v, cudaStream_t st);
 void launch_scan(uint32_t* a, int64_t L, uint32_t* part, cudaStream_t st, const LaunchHook& hook);
 void launch_fill(const Prm& P, cudaStream_t st);
-void launch_macros(const Prm& P, int slot, double fnum_vc, cudaStream_t st);
+void launch_macros(const Prm& P, const double* sums, int n_blocks, int m, double fnum_vc, cudaStream_t st);
 void launch_selftest_philox(int64_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out,
                             uint32_t* out_ref, cudaStream_t st);
 void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook);

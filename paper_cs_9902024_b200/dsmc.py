@@ -101,6 +101,8 @@ SIGNATURES = [
     ("dsmc_slot_samples", C.c_int, [_VP, C.c_int32, _VP]),
     ("dsmc_read_macros", C.c_int, [_VP, C.c_int32, _VP]),
     ("dsmc_read_sums", C.c_int, [_VP, C.c_int32, _VP]),
+    ("dsmc_slot_sums_ptr", C.c_int, [_VP, C.c_int32, C.POINTER(_VP)]),
+    ("dsmc_read_macros_gathered", C.c_int, [_VP, C.c_int32, _VP, C.c_int32, _VP]),
     ("dsmc_status", C.c_int, [_VP, _VP]),
     ("dsmc_get_state", C.c_int, [_VP, C.c_int32, C.POINTER(C.c_int64)] + [_VP] * 7),
     ("dsmc_set_state", C.c_int, [_VP, C.c_int32, C.c_int64] + [_VP] * 7 + [C.c_int32]),
@@ -243,6 +245,28 @@ class Simulation:
     def read_sums(self, slot):
         out = np.zeros((5, self.R, self.Nc), np.float64)
         _check(load_library().dsmc_read_sums(self.h, int(slot), _ptr(out)))
+        return out
+
+    def slot_sums_device(self, slot):
+        """The slot's sums [5][R*Nc] fp64 as a torch view of the caller-owned C buffer
+        (no copy): the send buffer of the one exchange (runs.gather_slot_sums)."""
+        import torch
+        ptr = C.c_void_p()
+        _check(load_library().dsmc_slot_sums_ptr(self.h, int(slot), C.byref(ptr)))
+        n = 5 * self.R * self.Nc
+        base = self.bufs["C"]
+        off = ptr.value - base.data_ptr()
+        assert off % 8 == 0 and off + 8 * n <= base.numel()
+        return base[off: off + 8 * n].view(torch.float64)
+
+    def read_macros_gathered(self, slot, sums_dev, n_blocks):
+        """Ensemble over n_blocks * R runs from device sums [n_blocks][5][R*Nc] (blocks in
+        ascending run id; e.g. an all-gather of every rank's slot_sums_device)."""
+        out = np.zeros((self.Nc, 10), np.float64)
+        assert sums_dev.is_cuda and sums_dev.dtype.itemsize == 8 and sums_dev.is_contiguous()
+        assert sums_dev.numel() == int(n_blocks) * 5 * self.R * self.Nc
+        _check(load_library().dsmc_read_macros_gathered(self.h, int(slot), C.c_void_p(sums_dev.data_ptr()),
+                                                        int(n_blocks), _ptr(out)))
         return out
 
     # --- status, checkpoint and test hooks

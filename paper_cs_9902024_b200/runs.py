@@ -47,6 +47,34 @@ def sum_over_ranks(value, group=None):
     return float(t.item())
 
 
+def gather_slot_sums(local, group=None):
+    """The one exchange, in the product's layout: `local` is this
+    rank's slot sums [5][n_local*Nc] fp64 (Simulation.slot_sums_device on a GPU, or
+    any tensor of that layout); returns [world][5][n_local*Nc] with block k = rank
+    k's, i.e. runs in ascending global run id when rank k owns runs [k*n, (k+1)*n)
+    (shard).  One all-gather over NCCL (NVLink) for device tensors, gloo for host
+    ones; feed the result to Simulation.read_macros_gathered."""
+    import torch
+    import torch.distributed as dist
+    local = local.contiguous()
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return local.reshape(1, *local.shape)
+    world = dist.get_world_size(group)
+    out = torch.empty((world, *local.shape), dtype=local.dtype, device=local.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, local, group=group)      # one NCCL all-gather into the block layout
+    else:                                                          # gloo: no _allgather_base
+        dist.all_gather(list(out.unbind(0)), local, group=group)
+    return out
+
+
+def ensemble_over_ranks(sim, slot, group=None):
+    """Ensemble macros of `slot` over the runs of every rank (bit-identical to one GPU
+    holding all of them): gather the slot sums, then dsmc_read_macros_gathered."""
+    g = gather_slot_sums(sim.slot_sums_device(slot), group)
+    return sim.read_macros_gathered(slot, g, g.shape[0])
+
+
 def gather_run_sums(local, group=None):
     """local: tensor [5][n_local][Nc] (float64) of this rank's runs (ascending
     run id).  Returns [5][n_local*world][Nc] on every rank, runs ordered by

@@ -89,3 +89,14 @@ def test_simulation_refuses_without_gpu(dsmc_mod):
         pytest.skip("GPU present")
     with pytest.raises(dsmc_mod.DsmcError):
         dsmc_mod.Simulation(configs.get("c4_small"))
+
+
+def test_too_many_runs_rejected(dsmc_mod):
+    """n_runs is the grid y dimension of the generation kernels (<= 65535): a larger
+    batch is rejected at validation with EINVAL, not by a failing launch later."""
+    p = configs.get("c1", n_runs=65536)
+    with pytest.raises(dsmc_mod.DsmcError) as e:
+        dsmc_mod.dsmc_query_sizes(p)
+    assert e.value.code == -1
+    p = configs.get("c1", n_runs=65535)
+    assert dsmc_mod.dsmc_query_sizes(p).n_cells == 100

@@ -57,6 +57,62 @@ def _worker(rank, world, port, out_path):
     dist.destroy_process_group()
 
 
+def _worker_slot_layout(rank, world, port, out_path):
+    """The exchange in the product's layout: each rank's slot sums as dsmc_read_sums /
+    Simulation.slot_sums_device lay them out, [5][n_local*Nc], gathered into
+    [world][5][n_local*Nc] by runs.gather_slot_sums (the input of
+    dsmc_read_macros_gathered)."""
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle
+    from paper_cs_9902024_b200 import runs
+    from workloads import configs
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    job = configs.get("c2_small", n_runs=6, n_steps=20)
+    mine = runs.shard(job, rank, world, runs_per_rank=3)
+    Nc = configs.n_cells(job)
+    snaps = []
+    for r in range(mine["run_id0"], mine["run_id0"] + mine["n_runs"]):
+        o = oracle.OracleRun(mine, r)
+        o.fill()
+        o.step(20)
+        snaps.append(o.get_snap(0))                                    # [5][Nc]
+    local = torch.from_numpy(np.array(snaps).transpose(1, 0, 2).reshape(5, 3 * Nc).copy())
+    g = runs.gather_slot_sums(local)
+    assert tuple(g.shape) == (world, 5, 3 * Nc)
+    if rank == 0:
+        per_run = g.numpy().reshape(world, 5, 3, Nc).transpose(0, 2, 1, 3).reshape(world * 3, 5, Nc)
+        np.savez(out_path, ens=oracle.ensemble(per_run, job["fnum_vc"]), per_run=per_run)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gather_in_product_layout(tmp_path, oracle_mod):
+    """runs.gather_slot_sums over gloo, world size 2: block k of the gathered tensor is
+    rank k's slot, so the runs come out in ascending global id and the ensemble of
+    the gathered sums equals the single-process ensemble over all 6 runs bit for bit."""
+    from workloads import configs
+    out = str(tmp_path / "g0.npz")
+    mp.spawn(_worker_slot_layout, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = np.load(out)
+    job = configs.get("c2_small", n_runs=6, n_steps=20)
+    sums = []
+    for r in range(6):
+        o = oracle_mod.OracleRun(job, r)
+        o.fill()
+        o.step(20)
+        sums.append(o.get_snap(0))
+    sums = np.array(sums)
+    assert np.array_equal(got["per_run"], sums)
+    want = oracle_mod.ensemble(sums, job["fnum_vc"])
+    assert np.array_equal(np.nan_to_num(got["ens"], nan=-7.0), np.nan_to_num(want, nan=-7.0))
+
+
 def test_two_rank_ensemble_equals_single(tmp_path, oracle_mod):
     from workloads import configs
     out = str(tmp_path / "r0.npz")
