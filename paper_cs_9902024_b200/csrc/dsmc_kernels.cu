@@ -31,6 +31,32 @@ namespace dsmc {
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr int DSMC_MODEL_HS = 0, DSMC_MODEL_VHS = 1;   // Prm::model
 
+// ------------------------------------------------------------- async copies
+// Bulk (TMA 1D) copy global -> shared completing on an mbarrier (sm_90+; SASS
+// UBLKCP / SYNCS), and 4-byte cp.async (LDGSTS) gathers that land in shared
+// memory without holding registers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+               " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ====================================================================== util
 __global__ void k_zero(uint32_t* __restrict__ a, int64_t n) {
   const int64_t n4 = n >> 2;
@@ -999,15 +1025,18 @@ struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
   uint32_t* cij; uint32_t* cur; float* cp; float* cq; float* ce; uint8_t* fl;
 };
 
+// the staged LCR slice `a` has 8 words of slack: the bulk copy moves the 16-byte
+// aligned window around [S, E) (up to 3 words on either side)
+constexpr int APAD = 8;
 __host__ __device__ inline size_t warp_smem_bytes(int capw) {
-  return (size_t)capw * 18 + (size_t)CCW * 21 + 16;
+  return (size_t)capw * 18 + 4 * APAD + (size_t)CCW * 21 + 16;
 }
 
 __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
   WarpSmem w;
   w.sorted = reinterpret_cast<uint32_t*>(base);
   w.a = w.sorted + capw;
-  w.vy = reinterpret_cast<float*>(w.a + capw);
+  w.vy = reinterpret_cast<float*>(w.a + capw + APAD);
   w.vz = w.vy + capw;
   w.cij = reinterpret_cast<uint32_t*>(w.vz + capw);
   w.cur = w.cij + CCW;
@@ -1133,6 +1162,7 @@ template <int D, int NET, int MODEL, bool STEP>
 __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int slot_arg, int capw) {
   const int mode = STEP ? 0 : mode_arg;      // STEP: the kernel of dsmc_step (mode 0) only
   extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ __align__(8) uint64_t s_bar;        // completion of the LCR slice's bulk copy (WPB == 1)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const WarpSmem W = warp_smem(dsm + (size_t)wid * warp_smem_bytes(capw), capw);
   const int64_t RN = (int64_t)P.R * P.Nc;
@@ -1184,29 +1214,41 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
   float gm = valid ? P.gmax[k] : 0.0f;
   const float gm0 = gm;
   if (cnt <= (uint32_t)capw) {
-    // ---- B (loads batched 8 deep per lane so their latencies overlap)
-    for (uint32_t q0 = 0; q0 < cnt; q0 += 256) {
-      uint32_t v[8];
-#pragma unroll
-      for (int u = 0; u < 8; u++) {
-        const uint32_t q = q0 + 32 * u + lane;
-        if (q < cnt) v[u] = P.lcr[S + q];
+    // ---- B: the tile's LCR slice [S, E) is contiguous: one lane moves its 16-byte
+    // aligned window into shared memory with a bulk (TMA) copy completing on an
+    // mbarrier, and the candidate counts of E0 (which need only N and the majorant)
+    // are drawn while it is in flight.  (The lcr buffer is a whole number of
+    // 32-slot run windows, so the window rounded up to 4 words stays inside it.)
+    uint32_t* const wa = W.a + (S & 3u);
+    if (cnt > 0) {
+      if (lane == 0) {
+        const uint32_t s0 = S & ~3u, e0 = (E + 3u) & ~3u;
+        mbar_init(&s_bar, 1u);
+        mbar_arrive_expect_tx(&s_bar, (e0 - s0) * 4u);
+        bulk_g2s(W.a, P.lcr + s0, (e0 - s0) * 4u, &s_bar);
       }
+      __syncwarp();
+    }
+    // ---- E0: candidate count M per cell (R12) and its exclusive warp prefix mst
+    uint32_t M = 0, mst = 0, tot = 0;
+    if (mode == 0) {
+      M = valid ? ntc_count(P, key, c, (uint32_t)s, N, gm) : 0u;
+      mst = M;
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
-        const uint32_t q = q0 + 32 * u + lane;
-        if (q < cnt) W.a[q] = v[u];
-      }
+      for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, mst, o); if (lane >= o) mst += y; }
+      tot = __shfl_sync(FULL, mst, 31);
+      mst -= M;
     }
     // largest segment of the warp (network width); element -> cell tags only
     // where the rank sort or the multi-run paths need them
     const uint32_t wN = __reduce_max_sync(FULL, valid ? N : 0u);
     if (valid && (wN > 32 || !one_run)) for (uint32_t i = 0; i < N; i++) W.cell[off + i] = (uint8_t)lane;
+    if (cnt > 0) mbar_wait(&s_bar, 0u);
     __syncwarp();
     // ---- C: network width by the warp's largest segment (warp-uniform)
     if (wN <= 32) {
       if (valid && N > 0) {
-        const uint32_t* src = W.a + off;
+        const uint32_t* src = wa + off;
         uint32_t* dst = W.sorted + off;
         if (wN <= 4) sort_segment<4, 4>(src, dst, N);
         else if (wN <= 8) sort_segment<8, 8>(src, dst, N);
@@ -1217,15 +1259,15 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
         else sort_segment<32, 32>(src, dst, N);
       }
     } else {
-      if (valid && N <= (uint32_t)NET) sort_segment<NET, NET>(W.a + off, W.sorted + off, N);
+      if (valid && N <= (uint32_t)NET) sort_segment<NET, NET>(wa + off, W.sorted + off, N);
       for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
         const uint32_t q = q0 + lane;
         const int cq = q < cnt ? W.cell[q] : 0;
         const uint32_t n = __shfl_sync(FULL, N, cq), b = __shfl_sync(FULL, off, cq);
         if (q < cnt && n > (uint32_t)NET) {
-          const uint32_t v = W.a[q];
+          const uint32_t v = wa[q];
           uint32_t rank = 0;
-          for (uint32_t p = 0; p < n; p++) rank += W.a[b + p] < v ? 1u : 0u;
+          for (uint32_t p = 0; p < n; p++) rank += wa[b + p] < v ? 1u : 0u;
           W.sorted[b + rank] = v;
         }
       }
@@ -1242,8 +1284,17 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
         uint32_t* m32 = reinterpret_cast<uint32_t*>(W.mod);
         for (uint32_t w = lane; w < (cnt + 3) / 4; w += 32) m32[w] = 0u;
       }
-      // gathers batched per lane (4 or 8 elements' loads issued before any store)
-      if (reo) {
+      // velocities in canonical order: 4-byte cp.async gathers straight into shared
+      // memory (no registers held while they are in flight); they complete while
+      // E1 draws the candidates, and the walk E2 waits for them
+      for (uint32_t q = lane; q < cnt; q += 32) {
+        const uint32_t g = W.sorted[q];
+        cp_async4(wvx + q, sx + g);
+        cp_async4(W.vy + q, sy + g);
+        cp_async4(W.vz + q, sz + g);
+      }
+      cp_async_commit();
+      if (reo) {   // positions to their canonical rank in the other half (loads batched 4 deep)
         const float* __restrict__ px = (h ? P1 : P0);
         const float* __restrict__ py = px + RS;
         const float* __restrict__ pz = py + RS;
@@ -1252,7 +1303,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
         float* __restrict__ dz = dy + RS;
         for (uint32_t q0 = 0; q0 < cnt; q0 += 128) {
           uint32_t gg[4];
-          float xs[4][D], vv[4][3];
+          float xs[4][D];
 #pragma unroll
           for (int u = 0; u < 4; u++) {
             const uint32_t q = q0 + 32 * u + lane;
@@ -1264,69 +1315,15 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
               xs[u][0] = px[gg[u]];
               if (D > 1) xs[u][D > 1 ? 1 : 0] = py[gg[u]];
               if (D > 2) xs[u][D > 2 ? 2 : 0] = pz[gg[u]];
-              vv[u][0] = sx[gg[u]];
-              vv[u][1] = sy[gg[u]];
-              vv[u][2] = sz[gg[u]];
             }
           }
 #pragma unroll
           for (int u = 0; u < 4; u++) {
             const uint32_t q = q0 + 32 * u + lane;
             if (q < cnt) {
-              wvx[q] = vv[u][0];
-              W.vy[q] = vv[u][1];
-              W.vz[q] = vv[u][2];
               dx[q] = xs[u][0];
               if (D > 1) dy[q] = xs[u][D > 1 ? 1 : 0];
               if (D > 2) dz[q] = xs[u][D > 2 ? 2 : 0];
-            }
-          }
-        }
-      } else {
-        // full 256-element rounds 8 deep without predicates, then the tail 2 deep
-        uint32_t q0 = 0;
-        for (; q0 + 256 <= cnt; q0 += 256) {
-          uint32_t gg[8];
-          float vv[8][3];
-#pragma unroll
-          for (int u = 0; u < 8; u++) gg[u] = W.sorted[q0 + 32 * u + lane];
-#pragma unroll
-          for (int u = 0; u < 8; u++) {
-            vv[u][0] = sx[gg[u]];
-            vv[u][1] = sy[gg[u]];
-            vv[u][2] = sz[gg[u]];
-          }
-#pragma unroll
-          for (int u = 0; u < 8; u++) {
-            const uint32_t q = q0 + 32 * u + lane;
-            wvx[q] = vv[u][0];
-            W.vy[q] = vv[u][1];
-            W.vz[q] = vv[u][2];
-          }
-        }
-        for (; q0 < cnt; q0 += 64) {
-          uint32_t gg[2];
-          float vv[2][3];
-#pragma unroll
-          for (int u = 0; u < 2; u++) {
-            const uint32_t q = q0 + 32 * u + lane;
-            gg[u] = q < cnt ? W.sorted[q] : 0u;
-          }
-#pragma unroll
-          for (int u = 0; u < 2; u++) {
-            if (q0 + 32 * u + lane < cnt) {
-              vv[u][0] = sx[gg[u]];
-              vv[u][1] = sy[gg[u]];
-              vv[u][2] = sz[gg[u]];
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 2; u++) {
-            const uint32_t q = q0 + 32 * u + lane;
-            if (q < cnt) {
-              wvx[q] = vv[u][0];
-              W.vy[q] = vv[u][1];
-              W.vz[q] = vv[u][2];
             }
           }
         }
@@ -1356,13 +1353,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
     __syncwarp();
     // ---- E
     if (mode == 0) {
-      const uint32_t M = valid ? ntc_count(P, key, c, (uint32_t)s, N, gm) : 0u;
       ncand = M;
-      uint32_t mst = M;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, mst, o); if (lane >= o) mst += y; }
-      const uint32_t tot = __shfl_sync(FULL, mst, 31);
-      mst -= M;                                   // exclusive prefix
       const uint32_t Mu = M, mstu = mst;
       const double gmu = (double)gm, ghatu = gmu / P.sigma_c;
       SmemCell Au{wvx + off, W.vy + off, W.vz + off, W.mod + off};
@@ -1375,6 +1366,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
           ntc_predraw<true, MODEL>(P, W, lane, base, lim, mst, N, ghatu, r, c, (uint32_t)s, run_key(P, r_first));
         else
           ntc_predraw<false, MODEL>(P, W, lane, base, lim, mst, N, ghatu, r, c, (uint32_t)s, run_key(P, r_first));
+        cp_async_wait_all();                      // the velocity gathers of D (pending in the first pass only)
         __syncwarp();
         if (Mu) {
           const uint32_t a0 = mstu > base ? mstu : base;
@@ -1392,6 +1384,8 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
         if (sgm > (double)gm) gm = (float)sgm;
       }
     }
+    cp_async_wait_all();                          // no candidates (or no Interaction): gathers of D
+    __syncwarp();
     const int slot = sched_slot(P, mode, s, slot_arg);
     if (valid && slot >= 0) sample_cell(P, slot, k, N, SmemCell{wvx + off, W.vy + off, W.vz + off, W.mod + off}, mode == 2);
     __syncwarp();
