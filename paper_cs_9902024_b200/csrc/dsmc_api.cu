@@ -43,7 +43,7 @@ struct Layout {
   int64_t Nc, stride, RN;
   int32_t n_face;
   // ctl offsets
-  size_t c_step, c_status, c_nstore, c_parity, c_reorder, c_inserted, c_counters, c_live, c_psteps, c_slot, c_queue, c_heavy,
+  size_t c_stepslot, c_step, c_status, c_nstore, c_parity, c_reorder, c_inserted, c_counters, c_live, c_psteps, c_slot, c_queue, c_heavy,
       c_items;
   // scratch offsets
   size_t s_face_j, s_face_k, s_open, s_kept, s_part, s_macros, s_heavy, s_cand, s_acc;
@@ -151,6 +151,7 @@ int make_layout(const dsmc_problem* p, int debug, Layout& L) {
   L.c_live = o; o = align_up(o + 8 * R, 16);
   L.c_psteps = o; o = align_up(o + 8 * R, 16);
   L.c_slot = o; o = align_up(o + 4 * (size_t)(s.n_slots > 0 ? s.n_slots : 1), 16);
+  L.c_stepslot = o; o = align_up(o + 4, 16);
   L.c_queue = o; o = align_up(o + 8 * 8, 16);
   L.c_items = o; o = align_up(o + 8 * ((size_t)R + 2), 16);
   L.c_heavy = o; o = align_up(o + 4 * 2 * dsmc::HEAVY_TIERS, 16);
@@ -248,6 +249,19 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   const dsmc_problem* p = prob;
   P.dim = p->dim; P.nx = p->nx; P.ny = p->ny; P.nz = p->nz;
   P.Nc = L.Nc; P.R = p->n_runs; P.stride = L.stride; P.cap = p->cap_per_run;
+  // magic divisor for run = key / Nc (keys < 2^31): l = ceil(log2 Nc), m = ceil(2^(31+l) / Nc) < 2^32,
+  // q = umulhi(k, m) >> (l - 1); exact since k * (m Nc - 2^(31+l)) < 2^31 Nc <= 2^(31+l)
+  if (L.Nc > 1) {
+    int l = 0;
+    while ((1ll << l) < L.Nc) l++;
+    const uint64_t m = ((1ull << (31 + l)) + (uint64_t)L.Nc - 1) / (uint64_t)L.Nc;
+    P.nc_mul = (uint32_t)m;
+    P.nc_shift = l - 1;
+    for (uint64_t kk : {(uint64_t)0, (uint64_t)L.Nc - 1, (uint64_t)L.Nc, (uint64_t)L.RN - 1, (uint64_t)0x7FFFFFFE}) {
+      const uint32_t q = (uint32_t)(((kk * m) >> 32) >> (l - 1));
+      if (kk < 0x80000000ull && q != kk / (uint64_t)L.Nc) { delete c; return fail(DSMC_EINVAL, "run divisor"); }
+    }
+  }
   P.half = 6 * (int64_t)p->n_runs * L.stride;
   P.seed = p->seed; P.run_id0 = (uint32_t)p->run_id0;
   P.dt_f = (float)p->dt;
@@ -346,6 +360,7 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   P.ctl.live = (int64_t*)(ct + L.c_live);
   P.ctl.psteps = (unsigned long long*)(ct + L.c_psteps);
   P.ctl.slot_done = (int32_t*)(ct + L.c_slot);
+  P.ctl.step_slot = (int32_t*)(ct + L.c_stepslot);
   P.ctl.queue = (unsigned long long*)(ct + L.c_queue);
   P.ctl.items = (int64_t*)(ct + L.c_items);
   P.ctl.heavy = (uint32_t*)(ct + L.c_heavy);

@@ -36,6 +36,7 @@ struct Ctl {
   int64_t* live;             // [R] live particles (after the last Indexing)
   unsigned long long* psteps;    // [R] sum over steps of live particles after Generation
   int32_t* slot_done;        // [n_slots]
+  int32_t* step_slot;        // [1] sample slot of the current step (R2), or -1 -- set by k_step_mid
   unsigned long long* queue; // [4][2] work-queue cursors (item, blocks done) per persistent kernel
   int64_t* items;            // [R+2] work items of the particle kernels: prefix over runs, total, items per
                              //       run if all runs hold as many (else 0) -- k_items
@@ -46,6 +47,8 @@ struct Prm {
   // grid / batch
   int32_t dim, nx, ny, nz;
   int64_t Nc;                // cells per run
+  uint32_t nc_mul;           // key / Nc = __umulhi(key, nc_mul) >> nc_shift for keys < 2^31 (nc_mul = 0: Nc = 1)
+  int32_t nc_shift;
   int32_t R;                 // runs in the batch
   int64_t stride;            // slots per run window
   int64_t cap;               // capacity per run
@@ -121,6 +124,12 @@ __device__ __forceinline__ uint4 philox(uint4 c, uint2 k) {
 __device__ __forceinline__ uint4 draw(uint2 key, uint32_t unit, uint32_t step, uint32_t tag, uint32_t sub,
                                       uint32_t block) {
   return philox(make_uint4(unit, step, (tag << 24) | (sub & 0xFFFFFFu), block), key);
+}
+
+// run of a (run, cell) key k < 2^31 (R*Nc < 2^31 is checked at create): k / Nc by a
+// multiply-shift (host-computed magic, exact for 31-bit dividends)
+__device__ __forceinline__ uint32_t run_of(const Prm& P, uint32_t k) {
+  return P.nc_mul ? __umulhi(k, P.nc_mul) >> P.nc_shift : k;
 }
 
 __device__ __forceinline__ uint2 run_key(const Prm& P, int r) { return make_uint2(P.seed, P.run_id0 + (uint32_t)r); }

@@ -649,6 +649,9 @@ __global__ void k_step_mid(Prm P) {
   P.ctl.inserted[r] = 0;
   const int K = P.reorder_every;
   P.ctl.reorder[r] = ((K > 0 && (s + 1) % K == 0) || (P.cap - n < P.insert_bound)) ? 1 : 0;
+  if (r == 0)   // Sampling of this step (R2: after step s when (s+1) is a multiple of the interval), or -1
+    *P.ctl.step_slot = ((s + 1) % P.sample_every == 0 && (s + 1) / P.sample_every - 1 < P.n_slots)
+                           ? (s + 1) / P.sample_every - 1 : -1;
 }
 
 __device__ __forceinline__ uint32_t run_lcr_base(const Prm& P, int r) {
@@ -1152,8 +1155,8 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
 // sample slot of this launch: the schedule's (R2: after step s when (s+1) is a
 // multiple of the sampling interval) in mode 0, the caller's otherwise
 __device__ __forceinline__ int sched_slot(const Prm& P, int mode, int32_t s, int slot_arg) {
-  if (mode != 0) return slot_arg;
-  return ((s + 1) % P.sample_every == 0 && (s + 1) / P.sample_every - 1 < P.n_slots) ? (s + 1) / P.sample_every - 1 : -1;
+  (void)s;
+  return mode != 0 ? slot_arg : *P.ctl.step_slot;   // k_step_mid decided it for this step
 }
 
 // MODEL: the collision model is a template parameter so that the hard-sphere
@@ -1176,8 +1179,8 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
   const int64_t klast = k0 + 31 < RN ? k0 + 31 : RN - 1;
   const int last_lane = (int)(klast - k0);
   const uint32_t Nc32 = (uint32_t)P.Nc;          // R*Nc < 2^31 (checked in dsmc_create)
-  const int r_first = (int)((uint32_t)k0 / Nc32);
-  const int r_last = (int)((uint32_t)klast / Nc32);
+  const int r_first = (int)run_of(P, (uint32_t)k0);
+  const int r_last = (int)run_of(P, (uint32_t)klast);
   const bool one_run = r_first == r_last;
   // ---- A
   uint32_t st = 0, en = 0;
@@ -1185,7 +1188,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
     st = k == 0 ? 0u : P.cell[k - 1];
     en = P.cell[k];
   }
-  const int r = valid ? (int)((uint32_t)k / Nc32) : r_last;
+  const int r = valid ? (int)run_of(P, (uint32_t)k) : r_last;
   const uint32_t c = valid ? (uint32_t)k - (uint32_t)r * Nc32 : 0u;
   const uint32_t N = en - st;
   const uint32_t S = __shfl_sync(FULL, st, 0);
@@ -1232,7 +1235,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
     // ---- E0: candidate count M per cell (R12) and its exclusive warp prefix mst
     uint32_t M = 0, mst = 0, tot = 0;
     if (mode == 0) {
-      M = valid ? ntc_count(P, key, c, (uint32_t)s, N, gm) : 0u;
+      M = valid ? ntc_count(P, one_run ? run_key(P, r_first) : key, c, (uint32_t)s, N, gm) : 0u;
       mst = M;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, mst, o); if (lane >= o) mst += y; }
@@ -1294,40 +1297,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
         cp_async4(W.vz + q, sz + g);
       }
       cp_async_commit();
-      if (reo) {   // positions to their canonical rank in the other half (loads batched 4 deep)
-        const float* __restrict__ px = (h ? P1 : P0);
-        const float* __restrict__ py = px + RS;
-        const float* __restrict__ pz = py + RS;
-        float* __restrict__ dx = (h ? P0 : P1) + (int64_t)r * P.stride + (S - rbase);
-        float* __restrict__ dy = dx + RS;
-        float* __restrict__ dz = dy + RS;
-        for (uint32_t q0 = 0; q0 < cnt; q0 += 128) {
-          uint32_t gg[4];
-          float xs[4][D];
-#pragma unroll
-          for (int u = 0; u < 4; u++) {
-            const uint32_t q = q0 + 32 * u + lane;
-            gg[u] = q < cnt ? W.sorted[q] : 0u;
-          }
-#pragma unroll
-          for (int u = 0; u < 4; u++) {
-            if (q0 + 32 * u + lane < cnt) {
-              xs[u][0] = px[gg[u]];
-              if (D > 1) xs[u][D > 1 ? 1 : 0] = py[gg[u]];
-              if (D > 2) xs[u][D > 2 ? 2 : 0] = pz[gg[u]];
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 4; u++) {
-            const uint32_t q = q0 + 32 * u + lane;
-            if (q < cnt) {
-              dx[q] = xs[u][0];
-              if (D > 1) dy[q] = xs[u][D > 1 ? 1 : 0];
-              if (D > 2) dz[q] = xs[u][D > 2 ? 2 : 0];
-            }
-          }
-        }
-      }
+      // (on reorder steps the positions move in F, once the staging arrays are free)
     } else {
       for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
         const uint32_t q = q0 + lane;
@@ -1392,13 +1362,34 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
     // ---- F
     if (one_run) {
       if (reo) {
-        float* __restrict__ dx = (h ? P0 : P1) + 3 * RS + (int64_t)r * P.stride + (S - rbase);
+        // the tile to its canonical rank in the other half: velocities from the
+        // staging arrays, then the positions gathered into them by cp.async (every
+        // load of the tile in flight at once) and written out the same way
+        float* __restrict__ dx = (h ? P0 : P1) + (int64_t)r * P.stride + (S - rbase);
         float* __restrict__ dy = dx + RS;
         float* __restrict__ dz = dy + RS;
         for (uint32_t q = lane; q < cnt; q += 32) {
+          dx[3 * RS + q] = wvx[q];
+          dy[3 * RS + q] = W.vy[q];
+          dz[3 * RS + q] = W.vz[q];
+        }
+        __syncwarp();
+        const float* __restrict__ px = (h ? P1 : P0);
+        const float* __restrict__ py = px + RS;
+        const float* __restrict__ pz = py + RS;
+        for (uint32_t q = lane; q < cnt; q += 32) {
+          const uint32_t g = W.sorted[q];
+          cp_async4(wvx + q, px + g);
+          if (D > 1) cp_async4(W.vy + q, py + g);
+          if (D > 2) cp_async4(W.vz + q, pz + g);
+        }
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
+        for (uint32_t q = lane; q < cnt; q += 32) {
           dx[q] = wvx[q];
-          dy[q] = W.vy[q];
-          dz[q] = W.vz[q];
+          if (D > 1) dy[q] = W.vy[q];
+          if (D > 2) dz[q] = W.vz[q];
         }
       } else {
         float* __restrict__ vxp = (h ? P1 : P0) + 3 * RS;
