@@ -775,6 +775,27 @@ __device__ __forceinline__ void pair_of(uint32_t w, uint32_t N, uint32_t& i, uin
 }
 
 // velocity accessors: shared-memory tile, or global memory through LCR
+// build-time A/B switches (tools/build_variant.sh passes -D): all give bit-identical results
+#ifndef DSMC_FULLWB
+// 1: F writes every velocity of the tile back (no collided flags to set, clear and
+// scan).  About 20% of the particles collide per step at c4, so ~83% of the 32-byte
+// sectors of the velocity arrays are written either way: the full write-back adds
+// ~20% DRAM writes and saves the flag work (c4 n=256: k_collide 12.35 -> 12.15 ms)
+#define DSMC_FULLWB 1
+#endif
+#ifndef DSMC_COLLIDE_MINB
+// __launch_bounds__ min blocks per SM of k_collide (1 warp per block): 16 caps it at
+// 128 registers, the most that keeps 16 warps per SM (130 registers: 15 warps, +3%)
+#define DSMC_COLLIDE_MINB 16
+#endif
+#ifndef DSMC_CCW
+#define DSMC_CCW 128        // pre-drawn candidates per pass of k_collide's E1
+#endif
+struct SmemCellNM {         // shared-memory cell without collided flags (DSMC_FULLWB)
+  float* vx; float* vy; float* vz;
+  __device__ void ld(uint32_t i, float a[3]) const { a[0] = vx[i]; a[1] = vy[i]; a[2] = vz[i]; }
+  __device__ void st(uint32_t i, const float a[3]) const { vx[i] = a[0]; vy[i] = a[1]; vz[i] = a[2]; }
+};
 struct SmemCell {
   float* vx; float* vy; float* vz; uint8_t* mod;
   __device__ void ld(uint32_t i, float a[3]) const { a[0] = vx[i]; a[1] = vy[i]; a[2] = vz[i]; }
@@ -1021,7 +1042,7 @@ __device__ void heap_sort(uint32_t* a, uint32_t n) {
 // mode 0: full step; mode 1: sample only into `slot_arg` (dsmc_sample);
 // mode 2: sample added to `slot_arg` (dsmc_sample_add, time averaging).
 constexpr int WPB = 1;      // warps per block (1: the tile index, hence run and key, is uniform)
-constexpr int CCW = 128;    // pre-drawn candidates per round per warp
+constexpr int CCW = DSMC_CCW;   // pre-drawn candidates per round per warp
 
 struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
   uint32_t* sorted; uint32_t* a; float* vy; float* vz; uint8_t* cell; uint8_t* mod;
@@ -1162,7 +1183,7 @@ __device__ __forceinline__ int sched_slot(const Prm& P, int mode, int32_t s, int
 // MODEL: the collision model is a template parameter so that the hard-sphere
 // kernel carries no VHS code (its presence cost 2.4% at c4)
 template <int D, int NET, int MODEL, bool STEP>
-__global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int slot_arg, int capw) {
+__global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, int mode_arg, int slot_arg, int capw) {
   const int mode = STEP ? 0 : mode_arg;      // STEP: the kernel of dsmc_step (mode 0) only
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ __align__(8) uint64_t s_bar;        // completion of the LCR slice's bulk copy (WPB == 1)
@@ -1285,7 +1306,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
       const float* __restrict__ sz = sy + RS;
       {  // clear the collided flags with word stores
         uint32_t* m32 = reinterpret_cast<uint32_t*>(W.mod);
-        for (uint32_t w = lane; w < (cnt + 3) / 4; w += 32) m32[w] = 0u;
+        if (!DSMC_FULLWB) for (uint32_t w = lane; w < (cnt + 3) / 4; w += 32) m32[w] = 0u;
       }
       // velocities in canonical order: 4-byte cp.async gathers straight into shared
       // memory (no registers held while they are in flight); they complete while
@@ -1326,7 +1347,11 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
       ncand = M;
       const uint32_t Mu = M, mstu = mst;
       const double gmu = (double)gm, ghatu = gmu / P.sigma_c;
+#if DSMC_FULLWB
+      SmemCellNM Au{wvx + off, W.vy + off, W.vz + off};
+#else
       SmemCell Au{wvx + off, W.vy + off, W.vz + off, W.mod + off};
+#endif
       float maxg2 = 0.0f;
       uint32_t naccu = 0;
       for (uint32_t base = 0; base < tot; base += CCW) {
@@ -1395,6 +1420,14 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
         float* __restrict__ vxp = (h ? P1 : P0) + 3 * RS;
         float* __restrict__ vyp = vxp + RS;
         float* __restrict__ vzp = vyp + RS;
+#if DSMC_FULLWB
+        for (uint32_t q = lane; q < cnt; q += 32) {
+          const uint32_t g = W.sorted[q];
+          vxp[g] = wvx[q];
+          vyp[g] = W.vy[q];
+          vzp[g] = W.vz[q];
+        }
+#else
         // collided flags read four at a time
         const uint32_t* m32 = reinterpret_cast<const uint32_t*>(W.mod);
         for (uint32_t w = lane; w < (cnt + 3) / 4; w += 32) {
@@ -1412,6 +1445,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
             }
           }
         }
+#endif
       }
     } else {
       for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
@@ -1426,7 +1460,7 @@ __global__ void __launch_bounds__(WPB * 32) k_collide(Prm P, int mode_arg, int s
             d[3 * RS] = wvx[q];
             d[4 * RS] = W.vy[q];
             d[5 * RS] = W.vz[q];
-          } else if (W.mod[q]) {
+          } else if (DSMC_FULLWB || W.mod[q]) {   // (full write-back: the walk sets no flags)
             float* d = (hq ? P1 : P0) + W.sorted[q];
             d[3 * RS] = wvx[q];
             d[4 * RS] = W.vy[q];
