@@ -366,10 +366,11 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   P.ctl.heavy = (uint32_t*)(ct + L.c_heavy);
   P.heavy_list = (uint32_t*)(sc + L.s_heavy);
   P.heavy_stride = (L.RN + 31) / 32 + 1;
-  // NEXT-1 A/B: DSMC_STATIC_CELLS=1 disables the heavy-tile queue, so
-  // overflowing tiles stay with their warp (lane = cell, global memory): the
-  // static mapping against which the TLPDPR-style reallocation is measured
-  if (const char* e = std::getenv("DSMC_STATIC_CELLS")) if (std::atoi(e)) P.heavy_list = nullptr;
+  // NEXT-1 A/B: DSMC_STATIC_CELLS=1 replaces the dynamic, size-tiered
+  // heavy-tile queue by a static block-per-tile mapping: every tile beyond the warp
+  // staging area goes to the large tier, dealt to its blocks round-robin -- the
+  // static mapping against which the TLPDPR-style reallocation (P:501-515) is measured
+  if (const char* e = std::getenv("DSMC_STATIC_CELLS")) if (std::atoi(e)) P.heavy_static = 1;
   P.caph = 8192;
   P.caph_tier[0] = 3584;      // 2 blocks per SM within the 196 KB carveout (4096: 215 KB, L1 down to 28 KB, 2-3% slower; a third tier of 1024, register-limited to 2 blocks too, measured slower)
   P.caph_tier[1] = P.caph;    // 1 block per SM

@@ -99,6 +99,7 @@ struct Prm {
   int32_t capw;              // particles a warp tile (32 cells) stages in shared memory
   int32_t caph;              // particles k_collide_heavy stages per tile
   uint32_t* heavy_list;      // [HEAVY_TIERS][heavy_stride] tiles k_collide handed to k_collide_heavy, by size tier
+  int32_t heavy_static;      // NEXT-1 A/B arm: one tier, tiles dealt to blocks round-robin (no queue)
   int64_t heavy_stride;      // entries per tier list (R*Nc/32 + 1)
   int32_t caph_tier[HEAVY_TIERS];   // staging capacity of each tier (the last one is caph)
   int64_t* dbg_cand;         // [R*Nc]

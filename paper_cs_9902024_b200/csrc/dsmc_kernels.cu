@@ -1225,19 +1225,20 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
   const int32_t s = *P.ctl.step;
   const uint2 key = run_key(P, r);
   uint32_t ncand = 0, nacc = 0;
-  if (cnt > (uint32_t)capw && P.heavy_list) {
+  if (cnt > (uint32_t)capw) {
     // tile too large for the warp's shared memory: hand it to k_collide_heavy
     // (a whole block with a large staging area -- the "heap" of TLPDPR)
-    // (tiered by size: the smaller the staging area, the more blocks per SM)
+    // (tiered by size: the smaller the staging area, the more blocks per SM;
+    // the static NEXT-1 arm puts every such tile in the large tier)
     if (lane == 0) {
-      const int q = cnt > (uint32_t)P.caph_tier[0] ? 1 : 0;      // HEAVY_TIERS == 2
+      const int q = (P.heavy_static || cnt > (uint32_t)P.caph_tier[0]) ? 1 : 0;      // HEAVY_TIERS == 2
       P.heavy_list[(int64_t)q * P.heavy_stride + atomicAdd(P.ctl.heavy + 2 * q, 1u)] = (uint32_t)(k0 / 32);
     }
     return;
   }
   float gm = valid ? P.gmax[k] : 0.0f;
   const float gm0 = gm;
-  if (cnt <= (uint32_t)capw) {
+  {
     // ---- B: the tile's LCR slice [S, E) is contiguous: one lane moves its 16-byte
     // aligned window into shared memory with a bulk (TMA) copy completing on an
     // mbarrier, and the candidate counts of E0 (which need only N and the majorant)
@@ -1471,26 +1472,6 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
     }
     if (P.debug)
       for (uint32_t q = lane; q < cnt; q += 32) P.lcr[S + q] = W.sorted[q];
-  } else if (valid) {
-    // tile too large for the warp's shared memory: each lane works on its
-    // own cell in global memory (segment sorted in place in LCR)
-    uint32_t* seg = P.lcr + st;
-    if (N <= 32) insertion_sort(seg, N);
-    else heap_sort(seg, N);
-    GlobCell A{seg, parr(P, h, 3), parr(P, h, 4), parr(P, h, 5)};
-    if (mode == 0) collide_cell(P, key, c, (uint32_t)s, N, A, gm, ncand, nacc);
-    const int slot = sched_slot(P, mode, s, slot_arg);
-    if (slot >= 0) sample_cell(P, slot, k, N, A, mode == 2);
-    if (reo) {
-      for (uint32_t i = 0; i < N; i++) {
-        const uint32_t g = seg[i];
-        const int64_t dst = (int64_t)r * P.stride + (int64_t)(st + i - rbase);
-#pragma unroll
-        for (int a = 0; a < D; a++) parr(P, h ^ 1, a)[dst] = parr(P, h, a)[g];
-#pragma unroll
-        for (int a = 3; a < 6; a++) parr(P, h ^ 1, a)[dst] = parr(P, h, a)[g];
-      }
-    }
   }
   if (valid && gm != gm0) P.gmax[k] = gm;
   if (valid && P.debug && mode == 0) { P.dbg_cand[k] = ncand; P.dbg_acc[k] = (int32_t)nacc; }
@@ -1554,9 +1535,11 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
   const uint32_t* const hlist = P.heavy_list + (int64_t)queue * P.heavy_stride;
   uint32_t* const hctr = P.ctl.heavy + 2 * queue;
   const uint32_t n_heavy = hctr[0];
-  for (;;) {
+  for (uint32_t it = 0;; it++) {
     __syncthreads();
-    if (t == 0) s_tile = atomicAdd(hctr + 1, 1u);
+    // dynamic: the next tile from the queue; static (NEXT-1 A/B arm): block b takes
+    // tiles b, b + G, b + 2G, ... whatever their sizes
+    if (t == 0) s_tile = P.heavy_static ? blockIdx.x + it * gridDim.x : atomicAdd(hctr + 1, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
     if (tile >= n_heavy) break;
