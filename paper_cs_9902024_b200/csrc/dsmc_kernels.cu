@@ -739,83 +739,6 @@ __global__ void __launch_bounds__(256) k_scatter(Prm P) {
   queue_done(P.ctl.queue + 2);
 }
 
-// Indexing with a shared-memory key window (build switch DSMC_SCATTER_WIN > 0): after
-// a reorder an item's keys are nearly sorted, so most fall in a window of WIN
-// consecutive (run, cell) keys around the item's middle key.  Those are ranked
-// in shared memory (one returning shared atomic per distinct key per 32-slice),
-// then each non-empty window cell reserves its LCR range with ONE global
-// atomic for the whole item; keys outside the window (long moves) take the
-// warp-aggregated global atomics of k_scatter.  The within-cell order stays
-// arbitrary (k_collide's phase C restores the canonical one).
-#ifndef DSMC_SCATTER_WIN
-#define DSMC_SCATTER_WIN 0
-#endif
-#if DSMC_SCATTER_WIN > 0
-constexpr int SW_T = 256, SW_PER = ITEM_S / SW_T;
-__global__ void __launch_bounds__(SW_T) k_scatter_w(Prm P) {
-  constexpr uint32_t WIN = DSMC_SCATTER_WIN;
-  __shared__ uint32_t s_cnt[WIN];
-  __shared__ uint32_t s_wbase;
-  __shared__ int64_t s_item;
-  const int t = threadIdx.x, lane = t & 31;
-  const unsigned lt = (1u << lane) - 1u;
-  const int64_t n_items = P.ctl.items[P.R];
-  for (int64_t item = queue_next(P.ctl.queue + 2, &s_item); item < n_items;
-       item = queue_next(P.ctl.queue + 2, &s_item)) {
-    const int r = item_run(P, item);
-    const int64_t n = P.ctl.n_store[r];
-    const int64_t ibase = (item - P.ctl.items[r]) * ITEM_S;
-    const int64_t base = (int64_t)r * P.stride;
-    const uint32_t* K = P.key + base;
-    const int64_t iend = ibase + ITEM_S < n ? ibase + ITEM_S : n;
-    for (uint32_t w = t; w < WIN; w += SW_T) s_cnt[w] = 0u;
-    if (t == 0) {   // window centred on the item's middle key (any choice is correct)
-      const int64_t mid = (ibase + iend) >> 1;
-      uint32_t km = K[mid];
-      if (km == DEAD_KEY) km = K[ibase];
-      s_wbase = km == DEAD_KEY ? 0u : (km > WIN / 2 ? km - WIN / 2 : 0u);
-    }
-    uint32_t kk[SW_PER];
-#pragma unroll
-    for (int j = 0; j < SW_PER; j++) {
-      const int64_t i = ibase + j * SW_T + t;
-      kk[j] = i < iend ? K[i] : DEAD_KEY;
-    }
-    __syncthreads();
-    const uint32_t wb = s_wbase;
-    uint32_t rk[SW_PER];
-    uint32_t glob = 0;                // bit j: rank rk[j] is already a global LCR position
-#pragma unroll
-    for (int j = 0; j < SW_PER; j++) {
-      const uint32_t key = kk[j];
-      const unsigned m = __match_any_sync(FULL, key);
-      const int ld = __ffs(m) - 1;
-      const bool inw = key - wb < WIN;
-      uint32_t old = 0;
-      if (key != DEAD_KEY && lane == ld)
-        old = inw ? atomicAdd(&s_cnt[key - wb], (uint32_t)__popc(m)) : atomicAdd(&P.cell[key], (uint32_t)__popc(m));
-      rk[j] = __shfl_sync(FULL, old, ld) + __popc(m & lt);
-      if (key != DEAD_KEY && !inw) glob |= 1u << j;
-    }
-    __syncthreads();
-    // one global atomic per non-empty window cell reserves the item's LCR range
-    for (uint32_t w = t; w < WIN; w += SW_T) {
-      const uint32_t c = s_cnt[w];
-      if (c) s_cnt[w] = atomicAdd(&P.cell[wb + w], c);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < SW_PER; j++) {
-      const uint32_t key = kk[j];
-      if (key == DEAD_KEY) continue;
-      const uint32_t pos = (glob >> j & 1u) ? rk[j] : s_cnt[key - wb] + rk[j];
-      P.lcr[pos] = (uint32_t)(base + ibase + j * SW_T + t);
-    }
-  }
-  queue_done(P.ctl.queue + 2);
-}
-#endif
-
 // ============================================================= Interaction
 // Isotropic direction, Marsaglia (reading R14): the first try from words z, w
 // of the candidate's pair block, further tries two per COLL_DIR block
@@ -2147,21 +2070,6 @@ void launch_items(const Prm& P, cudaStream_t st, bool motion) {
 }
 
 void launch_scatter(const Prm& P, cudaStream_t st) {
-#if DSMC_SCATTER_WIN > 0
-  {
-    static int occ_dev[MAX_DEV] = {0};
-    int& occ = occ_dev[cur_dev()];
-    if (!occ) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter_w, SW_T, 0);
-      if (occ < 1) occ = 1;
-    }
-    const int64_t items = (P.cap + ITEM_S - 1) / ITEM_S * P.R;
-    int64_t g = (int64_t)num_sms() * occ;
-    if (g > items) g = items;
-    k_scatter_w<<<(unsigned)g, SW_T, 0, st>>>(P);
-    return;
-  }
-#endif
   static int occ_dev[MAX_DEV] = {0};
   int& occ = occ_dev[cur_dev()];
   if (!occ) {
