@@ -304,9 +304,10 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
     int32_t ppc_max = 0;
     for (int k = 0; k < p->n_fill; k++) ppc_max = p->fill[k].ppc > ppc_max ? p->fill[k].ppc : ppc_max;
     if (p->inflow_kind == DSMC_INFLOW_GHOST) ppc_max = std::max(ppc_max, (int32_t)std::ceil(p->inflow_n));
-    // (5 sigma of the Poisson tile count: 4 blocks of 4 warps then stay under the
-    // 196 KB shared-memory carveout, which leaves the L1 the gathers need)
-    int32_t capw = 32 * ppc_max + 5 * (int32_t)std::ceil(std::sqrt(32.0 * ppc_max)) + 32;
+    // (3.5 sigma of the Poisson tile count: 16 one-warp blocks then stay under the
+    // 196 KB shared-memory carveout, which leaves the L1 the gathers need; the
+    // ~2e-4 of c4's tiles beyond it take the heavy blocks)
+    int32_t capw = 32 * ppc_max + (int32_t)std::ceil(3.5 * std::sqrt(32.0 * ppc_max));
     capw = std::max(256, std::min(capw, 4096));
     // an effusive source builds a dense plume the fills do not predict: tiles of a
     // few hundred particles are then common, and they are cheaper in the warp path

@@ -776,13 +776,11 @@ __device__ __forceinline__ void pair_of(uint32_t w, uint32_t N, uint32_t& i, uin
 
 // velocity accessors: shared-memory tile, or global memory through LCR
 // build-time A/B switches (tools/build_variant.sh passes -D): all give bit-identical results
-#ifndef DSMC_FULLWB
-// 1: F writes every velocity of the tile back (no collided flags to set, clear and
-// scan).  About 20% of the particles collide per step at c4, so ~83% of the 32-byte
-// sectors of the velocity arrays are written either way: the full write-back adds
-// ~20% DRAM writes and saves the flag work (c4 n=256: k_collide 12.35 -> 12.15 ms)
-#define DSMC_FULLWB 1
-#endif
+// k_collide's F writes every velocity of the tile back (no collided flags to set,
+// clear and scan).  About 20% of the particles collide per step at c4, so ~83% of
+// the 32-byte sectors of the velocity arrays are written either way: the full
+// write-back adds ~20% DRAM writes and saves the flag work (c4 n=256: k_collide
+// 12.35 -> 12.15 ms).
 #ifndef DSMC_COLLIDE_MINB
 // __launch_bounds__ min blocks per SM of k_collide (1 warp per block): 16 caps it at
 // 128 registers, the most that keeps 16 warps per SM (130 registers: 15 warps, +3%)
@@ -791,10 +789,10 @@ __device__ __forceinline__ void pair_of(uint32_t w, uint32_t N, uint32_t& i, uin
 #ifndef DSMC_CCW
 #define DSMC_CCW 128        // pre-drawn candidates per pass of k_collide's E1
 #endif
-struct SmemCellNM {         // shared-memory cell without collided flags (DSMC_FULLWB)
-  float* vx; float* vy; float* vz;
-  __device__ void ld(uint32_t i, float a[3]) const { a[0] = vx[i]; a[1] = vy[i]; a[2] = vz[i]; }
-  __device__ void st(uint32_t i, const float a[3]) const { vx[i] = a[0]; vy[i] = a[1]; vz[i] = a[2]; }
+struct SmemCell4 {          // shared-memory cell, velocities as float4 (x, y, z, -): one LDS.128 / STS.128
+  float4* v;
+  __device__ void ld(uint32_t i, float a[3]) const { const float4 t = v[i]; a[0] = t.x; a[1] = t.y; a[2] = t.z; }
+  __device__ void st(uint32_t i, const float a[3]) const { v[i] = make_float4(a[0], a[1], a[2], 0.0f); }
 };
 struct SmemCell {
   float* vx; float* vy; float* vz; uint8_t* mod;
@@ -909,23 +907,24 @@ __device__ __noinline__ void marsaglia_pq_from(uint2 key, uint32_t c, uint32_t s
 // candidates of one cell in increasing k with everything velocity-independent
 // drawn ahead (k_collide): ij = i | j << 16; thr = HS threshold F (accept iff
 // g2 > F) or the raw VHS acceptance word; (ex, ey, ez) the unit vector (R14)
+// rec[k] = (ex, ey, ez, threshold bits): one LDS.128 per candidate
 template <int MODEL, class A>
 __device__ __forceinline__ void ntc_apply_pre(const Prm& P, const A& acc, double gm, const uint32_t* ij,
-                                              const uint32_t* thr, const float* ex, const float* ey, const float* ez,
-                                              uint32_t n, float& maxg2, uint32_t& nacc) {
+                                              const float4* rec, uint32_t n, float& maxg2, uint32_t& nacc) {
   for (uint32_t k = 0; k < n; k++) {
     const uint32_t pr = ij[k];
     const uint32_t i = pr & 0xFFFFu, j = pr >> 16;
     float a[3], b[3];
     acc.ld(i, a);
     acc.ld(j, b);
+    const float4 rc = rec[k];
     const float dx = a[0] - b[0], dy = a[1] - b[1], dz = a[2] - b[2];
     const float g2 = (dx * dx + dy * dy) + dz * dz;
     maxg2 = g2 > maxg2 ? g2 : maxg2;
-    const bool accept = MODEL == DSMC_MODEL_HS ? g2 > __uint_as_float(thr[k])
-                                     : vhs_accept(P, thr[k], gm, g2);
+    const bool accept = MODEL == DSMC_MODEL_HS ? g2 > rc.w
+                                     : vhs_accept(P, __float_as_uint(rc.w), gm, g2);
     if (accept) {
-      const float e[3] = {ex[k], ey[k], ez[k]};
+      const float e[3] = {rc.x, rc.y, rc.z};
       const float cmx = (a[0] + b[0]) * 0.5f, cmy = (a[1] + b[1]) * 0.5f, cmz = (a[2] + b[2]) * 0.5f;
       const float hh = 0.5f * sqrtf(g2);
       const float pa[3] = {cmx + hh * e[0], cmy + hh * e[1], cmz + hh * e[2]};
@@ -1045,31 +1044,30 @@ constexpr int WPB = 1;      // warps per block (1: the tile index, hence run and
 constexpr int CCW = DSMC_CCW;   // pre-drawn candidates per round per warp
 
 struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
-  uint32_t* sorted; uint32_t* a; float* vy; float* vz; uint8_t* cell; uint8_t* mod;
-  uint32_t* cij; uint32_t* cur; float* cp; float* cq; float* ce; uint8_t* fl;
+  uint32_t* sorted;         // [capw] canonical (sorted) store indices of the tile
+  uint32_t* a;              // [capw + APAD] the staged LCR slice (aliases v4: dead after phase C)
+  float4* v4;               // [capw] velocities (x, y, z, -) in canonical order
+  float4* rec;              // [CCW] pre-drawn candidate: unit vector (R14) and acceptance threshold / word
+  uint32_t* cij;            // [CCW] candidate pair i | j << 16
+  uint8_t* cell; uint8_t* fl;
 };
 
 // the staged LCR slice `a` has 8 words of slack: the bulk copy moves the 16-byte
 // aligned window around [S, E) (up to 3 words on either side)
 constexpr int APAD = 8;
-__host__ __device__ inline size_t warp_smem_bytes(int capw) {
-  return (size_t)capw * 18 + 4 * APAD + (size_t)CCW * 21 + 16;
+__host__ __device__ inline size_t warp_smem_bytes(int capw) {   // capw a multiple of 32
+  return (size_t)capw * (4 + 16 + 1) + (size_t)CCW * (16 + 4 + 1) + 16;
 }
 
 __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
   WarpSmem w;
   w.sorted = reinterpret_cast<uint32_t*>(base);
-  w.a = w.sorted + capw;
-  w.vy = reinterpret_cast<float*>(w.a + capw + APAD);
-  w.vz = w.vy + capw;
-  w.cij = reinterpret_cast<uint32_t*>(w.vz + capw);
-  w.cur = w.cij + CCW;
-  w.cp = reinterpret_cast<float*>(w.cur + CCW);
-  w.cq = w.cp + CCW;
-  w.ce = w.cq + CCW;
-  w.cell = reinterpret_cast<uint8_t*>(w.ce + CCW);
-  w.mod = w.cell + capw;
-  w.fl = w.mod + capw;       // candidates whose first Marsaglia try was rejected
+  w.v4 = reinterpret_cast<float4*>(w.sorted + capw);        // 16-byte aligned (capw % 4 == 0)
+  w.a = reinterpret_cast<uint32_t*>(w.v4);                   // 4 capw + APAD words fit in 16 capw bytes
+  w.rec = w.v4 + capw;
+  w.cij = reinterpret_cast<uint32_t*>(w.rec + CCW);
+  w.cell = reinterpret_cast<uint8_t*>(w.cij + CCW);
+  w.fl = w.cell + capw;      // candidates whose first Marsaglia try was rejected
   return w;
 }
 
@@ -1124,19 +1122,20 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
           uint32_t i, j;
           pair_of(wp[hh].x, nc[hh], i, j);
           W.cij[q] = i | (j << 16);
+          uint32_t thr;
           if (MODEL == DSMC_MODEL_HS) {
             // HS: accept iff (double)g2 > (u ghat)^2 (R13)  <=>  g2 > F, F the largest
             // float <= (u ghat)^2 -- the same decision as one fp32 compare in the walk
             const double lhs = u_co_d(wp[hh].y) * gq_hat[hh];
-            W.cur[q] = __float_as_uint(__double2float_rd(lhs * lhs));
+            thr = __float_as_uint(__double2float_rd(lhs * lhs));
           } else {
-            W.cur[q] = wp[hh].y;
+            thr = wp[hh].y;
           }
           if (!fail) {   // unit vector of R14 from the pair block's try
             const float sr = sqrtf(1.0f - rho);
-            W.cp[q] = 2.0f * pp * sr;
-            W.cq[q] = 2.0f * qv * sr;
-            W.ce[q] = 1.0f - 2.0f * rho;
+            W.rec[q] = make_float4(2.0f * pp * sr, 2.0f * qv * sr, 1.0f - 2.0f * rho, __uint_as_float(thr));
+          } else {
+            reinterpret_cast<float*>(W.rec + q)[3] = __uint_as_float(thr);
           }
         }
       }
@@ -1166,9 +1165,10 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
         }
         const float rho = pp * pp + qv * qv;
         const float sr = sqrtf(1.0f - rho);
-        W.cp[q] = 2.0f * pp * sr;
-        W.cq[q] = 2.0f * qv * sr;
-        W.ce[q] = 1.0f - 2.0f * rho;
+        float* rq = reinterpret_cast<float*>(W.rec + q);
+        rq[0] = 2.0f * pp * sr;
+        rq[1] = 2.0f * qv * sr;
+        rq[2] = 1.0f - 2.0f * rho;
       }
     }
 }
@@ -1299,24 +1299,21 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
     }
     __syncwarp();
     // ---- D
-    float* const wvx = reinterpret_cast<float*>(W.a);
+    float4* const v4 = W.v4;
     if (one_run) {
       // per-array base pointers indexed by 32-bit offsets (one IMAD.WIDE per access)
       const float* __restrict__ sx = (h ? P1 : P0) + 3 * RS;
       const float* __restrict__ sy = sx + RS;
       const float* __restrict__ sz = sy + RS;
-      {  // clear the collided flags with word stores
-        uint32_t* m32 = reinterpret_cast<uint32_t*>(W.mod);
-        if (!DSMC_FULLWB) for (uint32_t w = lane; w < (cnt + 3) / 4; w += 32) m32[w] = 0u;
-      }
       // velocities in canonical order: 4-byte cp.async gathers straight into shared
       // memory (no registers held while they are in flight); they complete while
       // E1 draws the candidates, and the walk E2 waits for them
       for (uint32_t q = lane; q < cnt; q += 32) {
         const uint32_t g = W.sorted[q];
-        cp_async4(wvx + q, sx + g);
-        cp_async4(W.vy + q, sy + g);
-        cp_async4(W.vz + q, sz + g);
+        float* d = reinterpret_cast<float*>(v4 + q);
+        cp_async4(d, sx + g);
+        cp_async4(d + 1, sy + g);
+        cp_async4(d + 2, sz + g);
       }
       cp_async_commit();
       // (on reorder steps the positions move in F, once the staging arrays are free)
@@ -1335,10 +1332,7 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
 #pragma unroll
             for (int a = 0; a < D; a++) d[a * RS] = src[a * RS];
           }
-          wvx[q] = src[3 * RS];
-          W.vy[q] = src[4 * RS];
-          W.vz[q] = src[5 * RS];
-          W.mod[q] = 0;
+          v4[q] = make_float4(src[3 * RS], src[4 * RS], src[5 * RS], 0.0f);
         }
       }
     }
@@ -1348,11 +1342,7 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
       ncand = M;
       const uint32_t Mu = M, mstu = mst;
       const double gmu = (double)gm, ghatu = gmu / P.sigma_c;
-#if DSMC_FULLWB
-      SmemCellNM Au{wvx + off, W.vy + off, W.vz + off};
-#else
-      SmemCell Au{wvx + off, W.vy + off, W.vz + off, W.mod + off};
-#endif
+      SmemCell4 Au{v4 + off};
       float maxg2 = 0.0f;
       uint32_t naccu = 0;
       for (uint32_t base = 0; base < tot; base += CCW) {
@@ -1368,8 +1358,7 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
           const uint32_t a0 = mstu > base ? mstu : base;
           const uint32_t a1 = mstu + Mu < base + lim ? mstu + Mu : base + lim;
           if (a0 < a1)
-            ntc_apply_pre<MODEL>(P, Au, gmu, W.cij + (a0 - base), W.cur + (a0 - base), W.cp + (a0 - base),
-                          W.cq + (a0 - base), W.ce + (a0 - base), a1 - a0, maxg2, naccu);
+            ntc_apply_pre<MODEL>(P, Au, gmu, W.cij + (a0 - base), W.rec + (a0 - base), a1 - a0, maxg2, naccu);
         }
         __syncwarp();
       }
@@ -1383,7 +1372,7 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
     cp_async_wait_all();                          // no candidates (or no Interaction): gathers of D
     __syncwarp();
     const int slot = sched_slot(P, mode, s, slot_arg);
-    if (valid && slot >= 0) sample_cell(P, slot, k, N, SmemCell{wvx + off, W.vy + off, W.vz + off, W.mod + off}, mode == 2);
+    if (valid && slot >= 0) sample_cell(P, slot, k, N, SmemCell4{v4 + off}, mode == 2);
     __syncwarp();
     // ---- F
     if (one_run) {
@@ -1395,9 +1384,10 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
         float* __restrict__ dy = dx + RS;
         float* __restrict__ dz = dy + RS;
         for (uint32_t q = lane; q < cnt; q += 32) {
-          dx[3 * RS + q] = wvx[q];
-          dy[3 * RS + q] = W.vy[q];
-          dz[3 * RS + q] = W.vz[q];
+          const float4 v = v4[q];
+          dx[3 * RS + q] = v.x;
+          dy[3 * RS + q] = v.y;
+          dz[3 * RS + q] = v.z;
         }
         __syncwarp();
         const float* __restrict__ px = (h ? P1 : P0);
@@ -1405,48 +1395,31 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
         const float* __restrict__ pz = py + RS;
         for (uint32_t q = lane; q < cnt; q += 32) {
           const uint32_t g = W.sorted[q];
-          cp_async4(wvx + q, px + g);
-          if (D > 1) cp_async4(W.vy + q, py + g);
-          if (D > 2) cp_async4(W.vz + q, pz + g);
+          float* d = reinterpret_cast<float*>(v4 + q);
+          cp_async4(d, px + g);
+          if (D > 1) cp_async4(d + 1, py + g);
+          if (D > 2) cp_async4(d + 2, pz + g);
         }
         cp_async_commit();
         cp_async_wait_all();
         __syncwarp();
         for (uint32_t q = lane; q < cnt; q += 32) {
-          dx[q] = wvx[q];
-          if (D > 1) dy[q] = W.vy[q];
-          if (D > 2) dz[q] = W.vz[q];
+          const float4 v = v4[q];
+          dx[q] = v.x;
+          if (D > 1) dy[q] = v.y;
+          if (D > 2) dz[q] = v.z;
         }
       } else {
         float* __restrict__ vxp = (h ? P1 : P0) + 3 * RS;
         float* __restrict__ vyp = vxp + RS;
         float* __restrict__ vzp = vyp + RS;
-#if DSMC_FULLWB
         for (uint32_t q = lane; q < cnt; q += 32) {
           const uint32_t g = W.sorted[q];
-          vxp[g] = wvx[q];
-          vyp[g] = W.vy[q];
-          vzp[g] = W.vz[q];
+          const float4 v = v4[q];
+          vxp[g] = v.x;
+          vyp[g] = v.y;
+          vzp[g] = v.z;
         }
-#else
-        // collided flags read four at a time
-        const uint32_t* m32 = reinterpret_cast<const uint32_t*>(W.mod);
-        for (uint32_t w = lane; w < (cnt + 3) / 4; w += 32) {
-          const uint32_t m = m32[w];
-          if (m) {
-#pragma unroll
-            for (int b = 0; b < 4; b++) {
-              if (m & (0xFFu << (8 * b))) {
-                const uint32_t q = 4 * w + b;
-                const uint32_t g = W.sorted[q];
-                vxp[g] = wvx[q];
-                vyp[g] = W.vy[q];
-                vzp[g] = W.vz[q];
-              }
-            }
-          }
-        }
-#endif
       }
     } else {
       for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
@@ -1458,14 +1431,16 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
         if (q < cnt) {
           if (rq) {
             float* d = (hq ? P0 : P1) + (int64_t)runq * P.stride + (int64_t)(S + q - bq);
-            d[3 * RS] = wvx[q];
-            d[4 * RS] = W.vy[q];
-            d[5 * RS] = W.vz[q];
-          } else if (DSMC_FULLWB || W.mod[q]) {   // (full write-back: the walk sets no flags)
+            const float4 v = v4[q];
+            d[3 * RS] = v.x;
+            d[4 * RS] = v.y;
+            d[5 * RS] = v.z;
+          } else {                               // full write-back (no collided flags)
             float* d = (hq ? P1 : P0) + W.sorted[q];
-            d[3 * RS] = wvx[q];
-            d[4 * RS] = W.vy[q];
-            d[5 * RS] = W.vz[q];
+            const float4 v = v4[q];
+            d[3 * RS] = v.x;
+            d[4 * RS] = v.y;
+            d[5 * RS] = v.z;
           }
         }
       }
