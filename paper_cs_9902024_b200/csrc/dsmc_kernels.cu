@@ -786,6 +786,9 @@ __device__ __forceinline__ void pair_of(uint32_t w, uint32_t N, uint32_t& i, uin
 // 128 registers, the most that keeps 16 warps per SM (130 registers: 15 warps, +3%)
 #define DSMC_COLLIDE_MINB 16
 #endif
+#ifndef DSMC_NET_MAX
+#define DSMC_NET_MAX 32      // widest register network chosen by the warp's largest segment
+#endif
 #ifndef DSMC_CCW
 #define DSMC_CCW 128        // pre-drawn candidates per pass of k_collide's E1
 #endif
@@ -1052,9 +1055,8 @@ struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
   uint8_t* cell; uint8_t* fl;
 };
 
-// the staged LCR slice `a` has 8 words of slack: the bulk copy moves the 16-byte
-// aligned window around [S, E) (up to 3 words on either side)
-constexpr int APAD = 8;
+// the staged LCR slice `a` (the bulk copy's 16-byte aligned window around [S, E): up
+// to 3 words of slack on either side) aliases the 16 capw bytes of v4
 __host__ __device__ inline size_t warp_smem_bytes(int capw) {   // capw a multiple of 32
   return (size_t)capw * (4 + 16 + 1) + (size_t)CCW * (16 + 4 + 1) + 16;
 }
@@ -1267,11 +1269,11 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
     // largest segment of the warp (network width); element -> cell tags only
     // where the rank sort or the multi-run paths need them
     const uint32_t wN = __reduce_max_sync(FULL, valid ? N : 0u);
-    if (valid && (wN > 32 || !one_run)) for (uint32_t i = 0; i < N; i++) W.cell[off + i] = (uint8_t)lane;
+    if (valid && (wN > DSMC_NET_MAX || !one_run)) for (uint32_t i = 0; i < N; i++) W.cell[off + i] = (uint8_t)lane;
     if (cnt > 0) mbar_wait(&s_bar, 0u);
     __syncwarp();
     // ---- C: network width by the warp's largest segment (warp-uniform)
-    if (wN <= 32) {
+    if (wN <= DSMC_NET_MAX) {
       if (valid && N > 0) {
         const uint32_t* src = wa + off;
         uint32_t* dst = W.sorted + off;
@@ -1279,7 +1281,7 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
         else if (wN <= 8) sort_segment<8, 8>(src, dst, N);
         else if (wN <= 12) sort_segment<16, 12>(src, dst, N);
         else if (wN <= 16) sort_segment<16, 16>(src, dst, N);
-        else if (wN <= 20) sort_segment<32, 20>(src, dst, N);
+        else if (wN <= 20 || DSMC_NET_MAX <= 20) sort_segment<32, 20>(src, dst, N);
         else if (wN <= 24) sort_segment<32, 24>(src, dst, N);
         else sort_segment<32, 32>(src, dst, N);
       }
