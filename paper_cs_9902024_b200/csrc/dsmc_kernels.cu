@@ -382,7 +382,20 @@ __global__ void k_inflow_emit(Prm P) {
 // ================================================================= Motion
 // Full-accommodation diffuse re-emission (reading R10): Rayleigh normal speed
 // into the domain, N(0, T) tangential components, in fp64 then rounded.
-__device__ __forceinline__ void diffuse(uint2 key, uint32_t idx, uint32_t s, uint32_t b, int a, int sign, double sq,
+#ifndef DSMC_DIFFUSE_NOINLINE
+#define DSMC_DIFFUSE_NOINLINE 0
+#endif
+#ifndef DSMC_MOTION_EV_MINB
+// __launch_bounds__ min blocks/SM of k_motion with event surfaces: 4 caps it at 64 registers
+// (c5 after 300 steps: motion 0.75 -> 0.56 ms; c3: 2.01 -> 1.86 ms/step; 3 blocks: 0.62 ms)
+#define DSMC_MOTION_EV_MINB 4
+#endif
+#if DSMC_DIFFUSE_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+void diffuse(uint2 key, uint32_t idx, uint32_t s, uint32_t b, int a, int sign, double sq,
                                         float v[3]) {
   const uint4 w = draw(key, idx, s, TAG_WALL, b, 0);
   const double vn = sq * sqrt(-2.0 * log(u_oc_d(w.x)));
@@ -564,7 +577,7 @@ __device__ __forceinline__ uint32_t enumerate(const Prm& P, const float x[3], co
 // cells and the warp-aggregated histogram needs few atomics).
 // mode 0: move + enumerate, mode 1: enumerate only (explicit Sampling)
 template <int D, bool EV>
-__global__ void __launch_bounds__(256) k_motion(Prm P, int mode) {
+__global__ void __launch_bounds__(256, EV ? DSMC_MOTION_EV_MINB : 1) k_motion(Prm P, int mode) {
   const int lane = threadIdx.x & 31;
   const uint32_t s = (uint32_t)*P.ctl.step;
   const int64_t n_items = P.ctl.items[P.R];
