@@ -386,7 +386,8 @@ __global__ void k_inflow_emit(Prm P) {
 #define DSMC_DIFFUSE_NOINLINE 0
 #endif
 #ifndef DSMC_MOTION_EV_MINB
-// __launch_bounds__ min blocks/SM of k_motion with event surfaces: 4 caps it at 64 registers
+// __launch_bounds__ min blocks/SM of k_motion: 4 caps it at 64 registers (without the cap the
+// event-surface variants took 116; a min of 1 gave the plain c4 variant 80 registers, 4.40 -> 5.02 ms)
 // (c5 after 300 steps: motion 0.75 -> 0.56 ms; c3: 2.01 -> 1.86 ms/step; 3 blocks: 0.62 ms)
 #define DSMC_MOTION_EV_MINB 4
 #endif
@@ -577,7 +578,7 @@ __device__ __forceinline__ uint32_t enumerate(const Prm& P, const float x[3], co
 // cells and the warp-aggregated histogram needs few atomics).
 // mode 0: move + enumerate, mode 1: enumerate only (explicit Sampling)
 template <int D, bool EV>
-__global__ void __launch_bounds__(256, EV ? DSMC_MOTION_EV_MINB : 1) k_motion(Prm P, int mode) {
+__global__ void __launch_bounds__(256, EV ? DSMC_MOTION_EV_MINB : 0) k_motion(Prm P, int mode) {
   const int lane = threadIdx.x & 31;
   const uint32_t s = (uint32_t)*P.ctl.step;
   const int64_t n_items = P.ctl.items[P.R];
@@ -1388,6 +1389,9 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
     __syncwarp();
     const int slot = sched_slot(P, mode, s, slot_arg);
     if (valid && slot >= 0) sample_cell(P, slot, k, N, SmemCell4{v4 + off}, mode == 2);
+    // a tile without an accepted collision changed no velocity: nothing to write back
+    // on a non-reorder step (sparse tiles, e.g. c5's background)
+    const bool any_acc = __any_sync(FULL, nacc != 0);
     __syncwarp();
     // ---- F
     if (one_run) {
@@ -1424,7 +1428,7 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
           if (D > 1) dy[q] = v.y;
           if (D > 2) dz[q] = v.z;
         }
-      } else {
+      } else if (any_acc) {
         float* __restrict__ vxp = (h ? P1 : P0) + 3 * RS;
         float* __restrict__ vyp = vxp + RS;
         float* __restrict__ vzp = vyp + RS;
