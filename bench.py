@@ -191,6 +191,7 @@ def run_ours(args):
     _, st1 = sim.status()
     psteps = sum(b["particle_steps"] - a["particle_steps"] for a, b in zip(st0, st1))
     accepted = sum(b["accepted"] - a["accepted"] for a, b in zip(st0, st1)) / K
+    cands = sum(b["candidates"] - a["candidates"] for a, b in zip(st0, st1)) / K
     live_avg = psteps / K
     ms_max = runs.max_over_ranks(ms)
     psteps_all = runs.sum_over_ranks(float(psteps))
@@ -306,6 +307,7 @@ def run_ours(args):
                        "sample_every": S, "l2": "inputs larger than L2 (state %.1f GB)" % (
                            sum(getattr(sim.sizes, k) for k in ("P", "key", "lcr", "cell")) / 1e9),
                        "parallelism": f"runs sharded over {world} GPU(s), no collective"},
+            "collisions": {"accepted_per_step": accepted, "candidates_per_step": cands},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kps * K,
             "kernels_per_step": kps, "clocks": clk, "status": rc,
         }

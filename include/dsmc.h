@@ -186,8 +186,11 @@ int dsmc_read_macros_gathered(dsmc_ctx* ctx, int32_t slot, const double* sums_de
 
 /* SYNC. Returns the latched device fault (or OK); counters_out (may be NULL)
  * receives per run {inserted, removed, candidates, accepted, n_store, step,
- * live, particle_steps} as int64[n_runs][8]; particle_steps accumulates, per
- * step, the live particles after Generation (the bench metric's numerator). */
+ * live, particle_steps, max_ppc} as int64[n_runs][DSMC_STATUS_COLS];
+ * particle_steps accumulates, per step, the live particles after Generation
+ * (the bench metric's numerator); max_ppc is the largest particle count of one
+ * cell at the last Indexing (the cell-occupancy skew). */
+#define DSMC_STATUS_COLS 9
 int dsmc_status(dsmc_ctx* ctx, int64_t* counters_out);
 
 /* SYNC. Checkpoint / test hooks, host arrays in store order of run `run`.

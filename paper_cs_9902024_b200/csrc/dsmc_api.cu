@@ -11,6 +11,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "dsmc.h"
 #include "dsmc_device.cuh"
@@ -38,12 +39,18 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// NVTX range over one ABI call (host timeline of nsys / ncu --nvtx; no-ops without a tool)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
+
 struct Layout {
   dsmc_sizes sz;
   int64_t Nc, stride, RN;
   int32_t n_face;
   // ctl offsets
-  size_t c_stepslot, c_step, c_status, c_nstore, c_parity, c_reorder, c_inserted, c_counters, c_live, c_psteps, c_slot, c_queue, c_heavy,
+  size_t c_maxn, c_stepslot, c_step, c_status, c_nstore, c_parity, c_reorder, c_inserted, c_counters, c_live, c_psteps, c_slot, c_queue, c_heavy,
       c_items;
   // scratch offsets
   size_t s_face_j, s_face_k, s_open, s_kept, s_part, s_macros, s_heavy, s_cand, s_acc;
@@ -152,6 +159,7 @@ int make_layout(const dsmc_problem* p, int debug, Layout& L) {
   L.c_psteps = o; o = align_up(o + 8 * R, 16);
   L.c_slot = o; o = align_up(o + 4 * (size_t)(s.n_slots > 0 ? s.n_slots : 1), 16);
   L.c_stepslot = o; o = align_up(o + 4, 16);
+  L.c_maxn = o; o = align_up(o + 4 * R, 16);
   L.c_queue = o; o = align_up(o + 8 * 8, 16);
   L.c_items = o; o = align_up(o + 8 * ((size_t)R + 2), 16);
   L.c_heavy = o; o = align_up(o + 4 * 2 * dsmc::HEAVY_TIERS, 16);
@@ -362,6 +370,7 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   P.ctl.psteps = (unsigned long long*)(ct + L.c_psteps);
   P.ctl.slot_done = (int32_t*)(ct + L.c_slot);
   P.ctl.step_slot = (int32_t*)(ct + L.c_stepslot);
+  P.ctl.maxn = (uint32_t*)(ct + L.c_maxn);
   P.ctl.queue = (unsigned long long*)(ct + L.c_queue);
   P.ctl.items = (int64_t*)(ct + L.c_items);
   P.ctl.heavy = (uint32_t*)(ct + L.c_heavy);
@@ -439,6 +448,7 @@ int dsmc_destroy(dsmc_ctx* c) {
 
 int dsmc_generate(dsmc_ctx* c) {
   if (!c) return fail(DSMC_EINVAL, "null ctx");
+  Nvtx nv("dsmc_generate");
   dsmc::launch_fill(c->P, c->stream);
   CK(cudaGetLastError());
   return DSMC_OK;
@@ -446,6 +456,7 @@ int dsmc_generate(dsmc_ctx* c) {
 
 int dsmc_step(dsmc_ctx* c, int32_t nsteps) {
   if (!c || nsteps < 0) return fail(DSMC_EINVAL, "bad argument");
+  Nvtx nv("dsmc_step");
   for (int32_t i = 0; i < nsteps; i++) CK(cudaGraphLaunch(c->exec, c->stream));
   return DSMC_OK;
 }
@@ -457,8 +468,9 @@ struct TimedHook {
   cudaStream_t st;
   static void cb(void* u, int slot, int after) {
     TimedHook* h = (TimedHook*)u;
+    if (!after) nvtxRangePushA(dsmc::kernel_slot_name(slot));   // one NVTX range per kernel launch
     cudaEventRecord(h->ev[slot][after], h->st);
-    if (after) h->used[slot] = true;
+    if (after) { h->used[slot] = true; nvtxRangePop(); }
   }
 };
 }  // namespace
@@ -514,6 +526,7 @@ static int slot_written(dsmc_ctx* c, int32_t slot, bool* ok);
 
 int dsmc_sample(dsmc_ctx* c, int32_t slot) {
   if (!c) return fail(DSMC_EINVAL, "null ctx");
+  Nvtx nv("dsmc_sample");
   if (slot < 0 || slot >= c->L.sz.n_slots) return fail(DSMC_ESCHED, "slot out of range");
   dsmc::issue_sample(c->P, slot, 0, c->stream);
   CK(cudaGetLastError());
@@ -522,6 +535,7 @@ int dsmc_sample(dsmc_ctx* c, int32_t slot) {
 
 int dsmc_sample_add(dsmc_ctx* c, int32_t slot) {
   if (!c) return fail(DSMC_EINVAL, "null ctx");
+  Nvtx nv("dsmc_sample_add");
   if (slot < 0 || slot >= c->L.sz.n_slots) return fail(DSMC_ESCHED, "slot out of range");
   bool written = false;
   const int rc = slot_written(c, slot, &written);
@@ -558,6 +572,7 @@ static int slot_written(dsmc_ctx* c, int32_t slot, bool* ok) {
 
 // ensemble of n_blocks blocks of slot sums (block 0 may be this context's own slot) -> host out
 static int macros_from(dsmc_ctx* c, int32_t slot, const double* sums, int32_t n_blocks, double* out) {
+  Nvtx nv("dsmc_read_macros");
   int32_t m = 0;
   CK(cudaMemcpyAsync(&m, c->P.ctl.slot_done + slot, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -623,23 +638,27 @@ int dsmc_status(dsmc_ctx* c, int64_t* counters_out) {
   std::vector<unsigned long long> cnt(4 * (size_t)R);
   std::vector<int64_t> ns((size_t)R), live((size_t)R);
   std::vector<unsigned long long> ps((size_t)R);
+  std::vector<uint32_t> mx((size_t)R);
   int32_t step = 0;
   uint32_t stw = 0;
   CK(cudaMemcpyAsync(cnt.data(), c->P.ctl.counters, 8 * 4 * (size_t)R, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(ns.data(), c->P.ctl.n_store, 8 * (size_t)R, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(live.data(), c->P.ctl.live, 8 * (size_t)R, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(ps.data(), c->P.ctl.psteps, 8 * (size_t)R, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(mx.data(), c->P.ctl.maxn, 4 * (size_t)R, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(&step, c->P.ctl.step, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(&stw, c->P.ctl.status, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   const int32_t st = dsmc::status_code(stw);
   if (counters_out)
     for (int r = 0; r < R; r++) {
-      for (int q = 0; q < 4; q++) counters_out[r * 8 + q] = (int64_t)cnt[r * 4 + q];
-      counters_out[r * 8 + 4] = ns[r];
-      counters_out[r * 8 + 5] = step;
-      counters_out[r * 8 + 6] = live[r];
-      counters_out[r * 8 + 7] = (int64_t)ps[r];
+      int64_t* o = counters_out + (size_t)r * DSMC_STATUS_COLS;
+      for (int q = 0; q < 4; q++) o[q] = (int64_t)cnt[r * 4 + q];
+      o[4] = ns[r];
+      o[5] = step;
+      o[6] = live[r];
+      o[7] = (int64_t)ps[r];
+      o[8] = (int64_t)mx[r];
     }
   if (st) return fail(st, "latched device fault");
   return DSMC_OK;

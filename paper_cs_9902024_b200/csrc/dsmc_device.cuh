@@ -37,6 +37,7 @@ struct Ctl {
   unsigned long long* psteps;    // [R] sum over steps of live particles after Generation
   int32_t* slot_done;        // [n_slots]
   int32_t* step_slot;        // [1] sample slot of the current step (R2), or -1 -- set by k_step_mid
+  uint32_t* maxn;            // [R] largest particle count of one cell at the step's Indexing
   unsigned long long* queue; // [4][2] work-queue cursors (item, blocks done) per persistent kernel
   int64_t* items;            // [R+2] work items of the particle kernels: prefix over runs, total, items per
                              //       run if all runs hold as many (else 0) -- k_items

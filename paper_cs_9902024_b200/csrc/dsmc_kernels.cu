@@ -661,6 +661,7 @@ __global__ void k_step_mid(Prm P) {
   P.ctl.n_store[r] = n;
   P.ctl.psteps[r] += (unsigned long long)(P.ctl.live[r] + P.ctl.inserted[r]);
   P.ctl.inserted[r] = 0;
+  P.ctl.maxn[r] = 0u;          // k_collide takes the maximum over the step's cells
   const int K = P.reorder_every;
   P.ctl.reorder[r] = ((K > 0 && (s + 1) % K == 0) || (P.cap - n < P.insert_bound)) ? 1 : 0;
   if (r == 0)   // Sampling of this step (R2: after step s when (s+1) is a multiple of the interval), or -1
@@ -1241,6 +1242,13 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
   const int32_t s = *P.ctl.step;
   const uint2 key = run_key(P, r);
   uint32_t ncand = 0, nacc = 0;
+  // cell-occupancy skew: the step's largest particle count per cell, per run
+  if (one_run) {
+    const uint32_t wmax = __reduce_max_sync(FULL, valid ? N : 0u);
+    if (lane == 0 && wmax) atomicMax(P.ctl.maxn + r_first, wmax);
+  } else if (valid && N) {
+    atomicMax(P.ctl.maxn + r, N);
+  }
   if (cnt > (uint32_t)capw) {
     // tile too large for the warp's shared memory: hand it to k_collide_heavy
     // (a whole block with a large staging area -- the "heap" of TLPDPR)
@@ -2213,6 +2221,7 @@ void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
 
 void issue_sample(const Prm& P, int slot, int add, cudaStream_t st) {
   launch_zero(P.cell, (int64_t)P.R * P.Nc, st);
+  launch_zero(P.ctl.maxn, P.R, st);             // max_ppc of this Indexing
   launch_items(P, st, true);
   launch_motion(P, 1, st);
   launch_scan(P.cell, (int64_t)P.R * P.Nc, P.scan_part, st, LaunchHook{});

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(HERE, "libdsmc.so")
 DSMC_ERRORS = {0: "OK", -1: "EINVAL", -2: "ECLOCK", -3: "EPARAM", -4: "ECAP", -5: "EINDEX",
                -6: "ENONFINITE", -7: "ECUDA", -8: "ESCHED", -9: "EBOUNCE", -10: "ECELL"}
 MAX_KERNELS = 16
+STATUS_COLS = 9          # DSMC_STATUS_COLS of include/dsmc.h
 
 
 class DsmcError(RuntimeError):
@@ -271,11 +272,12 @@ class Simulation:
 
     # --- status, checkpoint and test hooks
     def status(self, raise_on_fault=True):
-        out = np.zeros((self.R, 8), np.int64)
+        out = np.zeros((self.R, STATUS_COLS), np.int64)
         rc = load_library().dsmc_status(self.h, _ptr(out))
         if raise_on_fault:
             _check(rc)
-        keys = ("inserted", "removed", "candidates", "accepted", "n_store", "step", "live", "particle_steps")
+        keys = ("inserted", "removed", "candidates", "accepted", "n_store", "step", "live", "particle_steps",
+                "max_ppc")
         return rc, [dict(zip(keys, map(int, row))) for row in out]
 
     def get_state(self, run):

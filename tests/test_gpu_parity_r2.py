@@ -17,7 +17,7 @@ from concurrent.futures import ProcessPoolExecutor
 import numpy as np
 import pytest
 
-from workloads import configs
+from workloads import configs, inputs
 
 from test_gpu_parity import compare_state, ensemble_compare
 
@@ -219,3 +219,35 @@ def test_gathered_ensemble_equals_single_context(dsmc_gpu, oracle_mod):
     out = np.zeros((whole.Nc, 10), np.float64)
     rc = dsmc_gpu.load_library().dsmc_read_macros_gathered(whole.h, 0, host.ctypes.data, 1, out.ctypes.data)
     assert rc == -1
+
+
+def test_max_particles_per_cell_counter(dsmc_gpu, oracle_mod):
+    """SURVEY §5 'max N per cell' (dsmc_status column max_ppc): the largest particle
+    count of one cell at the step's Indexing equals the oracle's max over its counts,
+    on a fill with heavy cells (tiles taken by k_collide_heavy) and on c5."""
+    p = configs.get("c4_small")
+    p["reorder_every"] = 1
+    p["fill"] = []
+    st = inputs.clustered_state(4, p, [5, 6, 7, 300, 301, 2000], 700)
+    p["cap_per_run"] = len(st["x"]) + 64
+    sim = dsmc_gpu.Simulation(p)
+    sim.generate()
+    for r in range(p["n_runs"]):
+        sim.set_state(r, st, step=0)
+    sim.step(1)
+    _, cnt = sim.status()
+    for r in range(p["n_runs"]):
+        ref = oracle_mod.OracleRun(p, r)
+        ref.set_state(st)
+        ref.step(1)
+        assert cnt[r]["max_ppc"] == int(ref.get_index()["count"].max()) > 500
+    q = configs.get("c5_small")
+    sim = dsmc_gpu.Simulation(q)
+    sim.generate()
+    sim.step(20)
+    _, cnt = sim.status()
+    for r in range(q["n_runs"]):
+        ref = oracle_mod.OracleRun(q, r)
+        ref.fill()
+        ref.step(20)
+        assert cnt[r]["max_ppc"] == int(ref.get_index()["count"].max())

@@ -1,5 +1,6 @@
-"""NEXT-1: the TLPDPR-style heavy-tile queue against a static
-lane-per-cell mapping on c5 once the orifice jet has built dense cells.
+"""NEXT-1: the TLPDPR-style heavy-tile queue (dynamic, two size tiers)
+against a static block-per-heavy-tile mapping (one tier, tiles dealt round-robin) on c5
+once the orifice jet has built dense cells.
 usage: python tools/heavy_ab.py WARM STEPS   (set DSMC_STATIC_CELLS=1 for the static arm)"""
 import json
 import os
