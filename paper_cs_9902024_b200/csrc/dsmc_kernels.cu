@@ -1199,7 +1199,10 @@ __device__ __forceinline__ int sched_slot(const Prm& P, int mode, int32_t s, int
 
 // MODEL: the collision model is a template parameter so that the hard-sphere
 // kernel carries no VHS code (its presence cost 2.4% at c4)
-template <int D, int NET, int MODEL, bool STEP>
+// ONE: every 32-cell tile lies in one run (Nc % 32 == 0 or a single run): the
+// multi-run paths are compiled out (c4: 6336 -> 5328 SASS instructions, k_collide
+// 12.15 -> 11.59 ms at n = 256, fewer instruction-cache misses)
+template <int D, int NET, int MODEL, bool STEP, bool ONE>
 __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, int mode_arg, int slot_arg, int capw) {
   const int mode = STEP ? 0 : mode_arg;      // STEP: the kernel of dsmc_step (mode 0) only
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -1219,7 +1222,7 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
   const uint32_t Nc32 = (uint32_t)P.Nc;          // R*Nc < 2^31 (checked in dsmc_create)
   const int r_first = (int)run_of(P, (uint32_t)k0);
   const int r_last = (int)run_of(P, (uint32_t)klast);
-  const bool one_run = r_first == r_last;
+  const bool one_run = ONE || r_first == r_last;
   // ---- A
   uint32_t st = 0, en = 0;
   if (valid) {
@@ -2099,7 +2102,7 @@ void launch_step_mid(const Prm& P, cudaStream_t st) {
   k_step_mid<<<(P.R + 127) / 128, 128, 0, st>>>(P);
 }
 
-template <int D, int NET, int MODEL, bool STEP>
+template <int D, int NET, int MODEL, bool STEP, bool ONE>
 static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t st) {
   const int64_t RN = (int64_t)P.R * P.Nc;
   const int64_t warps = (RN + 31) / 32;
@@ -2108,21 +2111,27 @@ static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t s
   static size_t configured_dev[MAX_DEV] = {0};
   size_t& configured = configured_dev[cur_dev()];
   if (smem > configured) {
-    cudaFuncSetAttribute(k_collide<D, NET, MODEL, STEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_collide<D, NET, MODEL, STEP, ONE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (const char* e = getenv("DSMC_CARVEOUT"))   // A/B experiments: shared-memory carveout (percent)
-      cudaFuncSetAttribute(k_collide<D, NET, MODEL, STEP>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
+      cudaFuncSetAttribute(k_collide<D, NET, MODEL, STEP, ONE>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
     configured = smem;
   }
-  k_collide<D, NET, MODEL, STEP><<<g, WPB * 32, smem, st>>>(P, mode, slot, capw);
+  k_collide<D, NET, MODEL, STEP, ONE><<<g, WPB * 32, smem, st>>>(P, mode, slot, capw);
 }
 
 template <int D, int NET>
 static void collide_m(const Prm& P, int mode, int slot, int capw, cudaStream_t st) {
   if (mode == 0) {
-    if (P.model == DSMC_MODEL_HS) collide_t<D, NET, DSMC_MODEL_HS, true>(P, mode, slot, capw, st);
-    else collide_t<D, NET, DSMC_MODEL_VHS, true>(P, mode, slot, capw, st);
+    const bool one = P.Nc % 32 == 0 || P.R == 1;    // no tile spans two runs
+    if (P.model == DSMC_MODEL_HS) {
+      if (one) collide_t<D, NET, DSMC_MODEL_HS, true, true>(P, mode, slot, capw, st);
+      else collide_t<D, NET, DSMC_MODEL_HS, true, false>(P, mode, slot, capw, st);
+    } else {
+      if (one) collide_t<D, NET, DSMC_MODEL_VHS, true, true>(P, mode, slot, capw, st);
+      else collide_t<D, NET, DSMC_MODEL_VHS, true, false>(P, mode, slot, capw, st);
+    }
   } else {   // explicit Sampling: no Interaction, so the model is irrelevant
-    collide_t<D, NET, DSMC_MODEL_HS, false>(P, mode, slot, capw, st);
+    collide_t<D, NET, DSMC_MODEL_HS, false, false>(P, mode, slot, capw, st);
   }
 }
 
