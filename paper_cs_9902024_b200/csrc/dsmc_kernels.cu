@@ -1302,12 +1302,15 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
       if (valid && N > 0) {
         const uint32_t* src = wa + off;
         uint32_t* dst = W.sorted + off;
-        if (wN <= 4) sort_segment<4, 4>(src, dst, N);
+#ifndef DSMC_NETS
+#define DSMC_NETS 5    // network widths: 8, 16, 20, 24, 32 (7 adds 4 and 12: c4 11.61 against 11.48-11.53 ms; c5 0.959 against 0.947)
+#endif
+        if (DSMC_NETS >= 7 && wN <= 4) sort_segment<4, 4>(src, dst, N);
         else if (wN <= 8) sort_segment<8, 8>(src, dst, N);
-        else if (wN <= 12) sort_segment<16, 12>(src, dst, N);
+        else if (DSMC_NETS >= 6 && wN <= 12) sort_segment<16, 12>(src, dst, N);
         else if (wN <= 16) sort_segment<16, 16>(src, dst, N);
         else if (wN <= 20 || DSMC_NET_MAX <= 20) sort_segment<32, 20>(src, dst, N);
-        else if (wN <= 24) sort_segment<32, 24>(src, dst, N);
+        else if (DSMC_NETS >= 5 && wN <= 24) sort_segment<32, 24>(src, dst, N);
         else sort_segment<32, 32>(src, dst, N);
       }
     } else {
