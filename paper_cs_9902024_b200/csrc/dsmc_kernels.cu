@@ -1291,6 +1291,13 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
       tot = __shfl_sync(FULL, mst, 31);
       mst -= M;
     }
+    const int slot = sched_slot(P, mode, s, slot_arg);
+    // a tile with no candidate, no Sampling and no reorder this step changes nothing
+    // (most of c5's sparse background): only the bulk copy is drained before the warp leaves
+    const bool idle = mode == 0 && tot == 0 && slot < 0 && !P.debug && __all_sync(FULL, reo == 0);
+    if (idle) {
+      if (cnt > 0) mbar_wait(&s_bar, 0u);
+    } else {
     // largest segment of the warp (network width); element -> cell tags only
     // where the rank sort or the multi-run paths need them
     const uint32_t wN = __reduce_max_sync(FULL, valid ? N : 0u);
@@ -1401,7 +1408,6 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
     }
     cp_async_wait_all();                          // no candidates (or no Interaction): gathers of D
     __syncwarp();
-    const int slot = sched_slot(P, mode, s, slot_arg);
     if (valid && slot >= 0) sample_cell(P, slot, k, N, SmemCell4{v4 + off}, mode == 2);
     // a tile without an accepted collision changed no velocity: nothing to write back
     // on a non-reorder step (sparse tiles, e.g. c5's background)
@@ -1480,6 +1486,7 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
     }
     if (P.debug)
       for (uint32_t q = lane; q < cnt; q += 32) P.lcr[S + q] = W.sorted[q];
+    }   // !idle
   }
   if (valid && gm != gm0) P.gmax[k] = gm;
   if (valid && P.debug && mode == 0) { P.dbg_cand[k] = ncand; P.dbg_acc[k] = (int32_t)nacc; }
