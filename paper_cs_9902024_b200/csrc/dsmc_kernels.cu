@@ -1719,36 +1719,41 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
           uint32_t* tmp = from; from = to; to = tmp;
         }
       }
-      // ---- D: gather velocities (and move positions on reorder steps)
-      for (uint32_t q0 = t; q0 < cnt; q0 += 4 * HT) {
-        float vx[4], vy[4], vz[4];
+      // ---- D: gather velocities by cp.async (they land while E0/E1 draw; the claim
+      // rounds wait for them), move positions on reorder steps
+      for (uint32_t q = t; q < cnt; q += HT) {
+        const int cq = s_cell[q];
+        const float* src = P.P + (int64_t)c_h[cq] * P.half + s_sorted[q];
+        cp_async4(s_vx + q, src + 3 * RS);
+        cp_async4(s_vy + q, src + 4 * RS);
+        cp_async4(s_vz + q, src + 5 * RS);
+        s_mod[q] = 0;
+        s_min[q] = 0xFFFFFFFFu;
+      }
+      cp_async_commit();
+      if (mode == 0) {
+        for (uint32_t q0 = t; q0 < cnt; q0 += 4 * HT) {
+          float xs[4][D];
+          int cqs[4];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const uint32_t q = q0 + u * HT;
-          if (q < cnt) {
-            const float* src = P.P + (int64_t)c_h[s_cell[q]] * P.half + s_sorted[q];
-            vx[u] = src[3 * RS];
-            vy[u] = src[4 * RS];
-            vz[u] = src[5 * RS];
+          for (int u = 0; u < 4; u++) {
+            const uint32_t q = q0 + u * HT;
+            cqs[u] = q < cnt ? s_cell[q] : 0;
+            if (q < cnt && c_reo[cqs[u]]) {
+              const float* src = P.P + (int64_t)c_h[cqs[u]] * P.half + s_sorted[q];
+#pragma unroll
+              for (int a = 0; a < D; a++) xs[u][a] = src[a * RS];
+            }
           }
-        }
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const uint32_t q = q0 + u * HT;
-          if (q < cnt) {
-            const int cq = s_cell[q];
-            if (c_reo[cq]) {
-              const int hq = c_h[cq];
-              const float* src = P.P + (int64_t)hq * P.half + s_sorted[q];
+          for (int u = 0; u < 4; u++) {
+            const uint32_t q = q0 + u * HT;
+            if (q < cnt && c_reo[cqs[u]]) {
+              const int cq = cqs[u], hq = c_h[cq];
               float* d = P.P + (int64_t)(hq ^ 1) * P.half + (int64_t)c_r[cq] * P.stride + (int64_t)(S + q - c_base[cq]);
 #pragma unroll
-              for (int a = 0; a < D; a++) d[a * RS] = src[a * RS];
+              for (int a = 0; a < D; a++) d[a * RS] = xs[u][a];
             }
-            s_vx[q] = vx[u];
-            s_vy[q] = vy[u];
-            s_vz[q] = vz[u];
-            s_mod[q] = 0;
-            s_min[q] = 0xFFFFFFFFu;
           }
         }
       }
@@ -1799,6 +1804,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
             s_cp[q] = pp;
             s_cq[q] = qv;
           }
+          if (base == 0) cp_async_wait_all();       // the velocity gathers of D
           __syncthreads();
           // dependency rounds: an undone candidate claims both its particles
           // (atomicMin of its index) and runs once it is the earliest undone
@@ -1871,6 +1877,8 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
           if (sgm > gmd) gm = (float)sgm;
         }
       }
+      cp_async_wait_all();                          // no candidates (or no Interaction): gathers of D
+      __syncthreads();
       if (valid && slot >= 0) {
         const uint32_t off = c_st[t] - S;
         sample_cell(P, slot, k0 + t, N, SmemCell{s_vx + off, s_vy + off, s_vz + off, s_mod + off}, mode == 2);
