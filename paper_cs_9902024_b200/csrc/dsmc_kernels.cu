@@ -1275,6 +1275,7 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
     if (cnt > 0) {
       if (lane == 0) {
         const uint32_t s0 = S & ~3u, e0 = (E + 3u) & ~3u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes before the async copy
         mbar_init(&s_bar, 1u);
         mbar_arrive_expect_tx(&s_bar, (e0 - s0) * 4u);
         bulk_g2s(W.a, P.lcr + s0, (e0 - s0) * 4u, &s_bar);
@@ -1536,6 +1537,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
   __shared__ float c_gm[32];
   __shared__ double c_gh[32];
   __shared__ uint32_t s_tile, c_k[33], s_nmax;
+  __shared__ __align__(8) uint64_t s_hbar;       // completion of the tile's LCR bulk copy
   const int t = threadIdx.x;
   const int64_t RN = (int64_t)P.R * P.Nc;
   const int64_t RS = (int64_t)P.R * P.stride;
@@ -1550,6 +1552,8 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
   const uint32_t* const hlist = P.heavy_list + (int64_t)queue * P.heavy_stride;
   uint32_t* const hctr = P.ctl.heavy + 2 * queue;
   const uint32_t n_heavy = hctr[0];
+  if (t == 0) mbar_init(&s_hbar, 1u);            // initialised once; each staged tile completes one phase
+  uint32_t hphase = 0;
   for (uint32_t it = 0;; it++) {
     __syncthreads();
     // dynamic: the next tile from the queue; static (NEXT-1 A/B arm): block b takes
@@ -1607,27 +1611,32 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
     const float gm0 = gm;
     uint32_t ncand = 0, nacc = 0;
     if (cnt <= (uint32_t)caph) {
-      // ---- B: stage the LCR slice, tag each element with its cell
-      // (this and the loops of C and D take four elements per thread at a time:
-      // independent load and search chains overlap)
-      for (uint32_t q0 = t; q0 < cnt; q0 += 4 * HT) {
-        uint32_t v[4];
+      // ---- B: the tile's LCR slice is contiguous: one thread moves its 16-byte aligned
+      // window into shared memory with a bulk copy on an mbarrier while the block tags
+      // every element with its cell.  It lands in the buffer the chunk sort of C does
+      // not write (C reads it at offset S & 3); the window's up-to-3-word overhang
+      // past cnt spills into the next buffer, which C or D overwrites afterwards.
+      int nlev = 0;
+      for (uint32_t L = 64; L < s_nmax; L <<= 1) nlev++;
+      uint32_t* const stage = (nlev & 1) ? s_sorted : s_a;   // C's chunk sort writes the other one
+      if (t == 0 && cnt > 0) {
+        const uint32_t s0 = S & ~3u, e0 = (E + 3u) & ~3u;
+        // the previous tile's generic-proxy writes to this shared memory (ordered by the
+        // block barriers since) must be ordered before the bulk copy's async-proxy writes
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(&s_hbar, (e0 - s0) * 4u);
+        bulk_g2s(stage, P.lcr + s0, (e0 - s0) * 4u, &s_hbar);
+      }
+      for (uint32_t q = t; q < cnt; q += HT) {
+        int lo = 0;
 #pragma unroll
-        for (int u = 0; u < 4; u++) if (q0 + u * HT < cnt) v[u] = P.lcr[S + q0 + u * HT];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const uint32_t q = q0 + u * HT;
-          if (q < cnt) {
-            s_a[q] = v[u];
-            int lo = 0;
-#pragma unroll
-            for (int stp = 16; stp > 0; stp >>= 1)
-              if (lo + stp <= last && c_st[lo + stp] <= S + q) lo += stp;
-            s_cell[q] = (uint8_t)lo;
-          }
-        }
+        for (int stp = 16; stp > 0; stp >>= 1)
+          if (lo + stp <= last && c_st[lo + stp] <= S + q) lo += stp;
+        s_cell[q] = (uint8_t)lo;
       }
       __syncthreads();
+      if (cnt > 0) { mbar_wait(&s_hbar, hphase); hphase ^= 1u; }   // one phase per staged tile
+      const uint32_t* const s_in = stage + (S & 3u);
       // ---- C: sort every cell's segment: a warp bitonic sort of each 64-element
       // chunk, then merge rounds in which every element finds its place by a
       // binary search of the partner run (keys are distinct store slots).  An
@@ -1636,8 +1645,6 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
       // slower than that.
       {
         const uint32_t nmax = s_nmax;
-        int nlev = 0;
-        for (uint32_t L = 64; L < nmax; L <<= 1) nlev++;
         uint32_t* from = (nlev & 1) ? s_a : s_sorted;   // the last round lands in s_sorted
         const int ln = t & 31;
         const uint32_t nchk = c_k[32];
@@ -1648,7 +1655,7 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
             if (lo + stp < 32 && c_k[lo + stp] <= ch) lo += stp;
           const uint32_t b = c_st[lo] - S + ((ch - c_k[lo]) << 6), n = c_st[lo] - S + c_N[lo];
           const bool in0 = b + ln < n, in1 = b + 32 + ln < n;
-          uint32_t x0 = in0 ? s_a[b + ln] : 0xFFFFFFFFu, x1 = in1 ? s_a[b + 32 + ln] : 0xFFFFFFFFu;
+          uint32_t x0 = in0 ? s_in[b + ln] : 0xFFFFFFFFu, x1 = in1 ? s_in[b + 32 + ln] : 0xFFFFFFFFu;
           // 64-element bitonic sort, element e = lane + 32 h in x_h
 #pragma unroll
           for (int k = 2; k <= 64; k <<= 1)
