@@ -402,10 +402,20 @@ void diffuse(uint2 key, uint32_t idx, uint32_t s, uint32_t b, int a, int sign, d
   const double vn = sq * sqrt(-2.0 * log(u_oc_d(w.x)));
   double t1, t2;
   box_muller(w.y, w.z, t1, t2);
-  const int c1 = a == 0 ? 1 : 0, c2 = a == 2 ? 1 : 2;
-  v[a] = (float)(sign > 0 ? vn : -vn);
-  v[c1] = (float)(0.0 + sq * t1);
-  v[c2] = (float)(0.0 + sq * t2);
+  // normal component on axis a, the tangential ones in axis order (selects: a runtime
+  // index into v[] would put the particle's registers in local memory)
+  const float fn = (float)(sign > 0 ? vn : -vn), f1 = (float)(0.0 + sq * t1), f2 = (float)(0.0 + sq * t2);
+  v[0] = a == 0 ? fn : f1;
+  v[1] = a == 1 ? fn : (a == 0 ? f1 : f2);
+  v[2] = a == 2 ? fn : f2;
+}
+
+// component a (runtime) of a 3-vector, and its assignment, without dynamic indexing
+__device__ __forceinline__ float comp(const float x[3], int a) { return a == 0 ? x[0] : (a == 1 ? x[1] : x[2]); }
+__device__ __forceinline__ void set_comp(float x[3], int a, float val) {
+  x[0] = a == 0 ? val : x[0];
+  x[1] = a == 1 ? val : x[1];
+  x[2] = a == 2 ? val : x[2];
 }
 
 // Motion with surface interaction (reading R10).  Returns
@@ -440,11 +450,11 @@ __device__ __forceinline__ bool move_one(const Prm& P, uint2 key, uint32_t idx, 
       if (D == 2 && P.plate_on) {
         const int pa = P.plate_axis, qa = P.plate_span_axis;
         const float pc = P.plate_pos;
-        s0 = x[pa] >= pc;
-        const bool s1 = x1[pa] >= pc;
+        s0 = comp(x, pa) >= pc;
+        const bool s1 = comp(x1, pa) >= pc;
         if (s0 != s1) {
-          const float t = (pc - x[pa]) / v[pa];
-          const float xq = fmaf(v[qa], t, x[qa]);
+          const float t = (pc - comp(x, pa)) / comp(v, pa);
+          const float xq = fmaf(comp(v, qa), t, comp(x, qa));
           if (xq >= P.plate_lo && xq <= P.plate_hi && t < tbest) { tbest = t; ev = 6; }
         }
       }
@@ -459,7 +469,7 @@ __device__ __forceinline__ bool move_one(const Prm& P, uint2 key, uint32_t idx, 
         if (bc == BC_OUTFLOW || bc == BC_INFLOW) return true;
 #pragma unroll
         for (int c = 0; c < D; c++) if (c != a) x[c] = fmaf(v[c], t, x[c]);
-        x[a] = f ? (float)axis_n(P, a) : 0.0f;
+        set_comp(x, a, f ? (float)axis_n(P, a) : 0.0f);
         if (D == 3 && P.orifice_on && a == 0 && f == 0) {
           int32_t j = (int32_t)floorf(x[1]), k = (int32_t)floorf(x[2]);
           j = j < 0 ? 0 : (j > P.ny - 1 ? P.ny - 1 : j);
@@ -473,7 +483,7 @@ __device__ __forceinline__ bool move_one(const Prm& P, uint2 key, uint32_t idx, 
         const float pc = P.plate_pos;
 #pragma unroll
         for (int c = 0; c < D; c++) if (c != pa) x[c] = fmaf(v[c], t, x[c]);
-        x[pa] = s0 ? pc : nextafterf(pc, -__int_as_float(0x7f800000));
+        set_comp(x, pa, s0 ? pc : nextafterf(pc, -__int_as_float(0x7f800000)));
         if (b == MAX_BOUNCE) { latch(P, ST_BOUNCE); break; }
         diffuse(key, idx, s, (uint32_t)b, pa, s0 ? 1 : -1, P.sqrt_plateT, v);
       }
