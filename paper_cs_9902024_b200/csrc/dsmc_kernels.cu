@@ -1239,7 +1239,7 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
     st = k == 0 ? 0u : P.cell[k - 1];
     en = P.cell[k];
   }
-  const int r = valid ? (int)run_of(P, (uint32_t)k) : r_last;
+  const int r = ONE ? r_first : (valid ? (int)run_of(P, (uint32_t)k) : r_last);
   const uint32_t c = valid ? (uint32_t)k - (uint32_t)r * Nc32 : 0u;
   const uint32_t N = en - st;
   const uint32_t S = __shfl_sync(FULL, st, 0);
@@ -1296,11 +1296,13 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
     uint32_t M = 0, mst = 0, tot = 0;
     if (mode == 0) {
       M = valid ? ntc_count(P, one_run ? run_key(P, r_first) : key, c, (uint32_t)s, N, gm) : 0u;
-      mst = M;
+      tot = __reduce_add_sync(FULL, M);
+      if (tot) {                                 // (an idle tile needs no prefix)
+        mst = M;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, mst, o); if (lane >= o) mst += y; }
-      tot = __shfl_sync(FULL, mst, 31);
-      mst -= M;
+        for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, mst, o); if (lane >= o) mst += y; }
+        mst -= M;
+      }
     }
     const int slot = sched_slot(P, mode, s, slot_arg);
     // a tile with no candidate, no Sampling and no reorder this step changes nothing
@@ -1502,7 +1504,18 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
   if (valid && gm != gm0) P.gmax[k] = gm;
   if (valid && P.debug && mode == 0) { P.dbg_cand[k] = ncand; P.dbg_acc[k] = (int32_t)nacc; }
   // per-run counters: aggregate lanes of the same run
-  if (mode == 0) {
+  if (ONE) {
+    if (mode == 0) {
+      const uint32_t sc = __reduce_add_sync(FULL, ncand);
+      if (sc) {
+        const uint32_t sa = __reduce_add_sync(FULL, nacc);
+        if (lane == 0) {
+          atomicAdd(&P.ctl.counters[r_first * 4 + 2], (unsigned long long)sc);
+          atomicAdd(&P.ctl.counters[r_first * 4 + 3], (unsigned long long)sa);
+        }
+      }
+    }
+  } else if (mode == 0) {
     const uint32_t rk = valid ? (uint32_t)r : 0xFFFFFFFFu;
     const unsigned m = __match_any_sync(FULL, rk);
     const uint32_t sc = __reduce_add_sync(m, ncand), sa = __reduce_add_sync(m, nacc);
