@@ -100,3 +100,14 @@ def test_too_many_runs_rejected(dsmc_mod):
     assert e.value.code == -1
     p = configs.get("c1", n_runs=65535)
     assert dsmc_mod.dsmc_query_sizes(p).n_cells == 100
+
+
+def test_32bit_key_overflow_rejected(dsmc_mod):
+    """Keys and LCR entries are 32-bit (run * Nc + cell, run * stride + i): a batch whose
+    slots reach 2^32 is rejected at validation (EINVAL), never wrapped silently."""
+    p = configs.get("c4", n_runs=1700)               # 1700 * 2,621,440 slots > 2^32
+    with pytest.raises(dsmc_mod.DsmcError) as e:
+        dsmc_mod.dsmc_query_sizes(p)
+    assert e.value.code == -1
+    p = configs.get("c4", n_runs=1600)               # 4.19e9 < 2^32 - 1: accepted
+    assert dsmc_mod.dsmc_query_sizes(p).n_cells == 64 ** 3

@@ -251,3 +251,31 @@ def test_max_particles_per_cell_counter(dsmc_gpu, oracle_mod):
         ref.fill()
         ref.step(20)
         assert cnt[r]["max_ppc"] == int(ref.get_index()["count"].max())
+
+
+def test_empty_store_steps_and_samples(dsmc_gpu, oracle_mod):
+    """Degenerate input: no particle at all (no fill, no inflow).  Every kernel sees
+    empty cells and empty tiles; steps, Sampling and the ensemble must still run:
+    zero counters, zero sums, density 0 and NaN velocity/temperature (R18: S_N = 0),
+    exactly as the oracle."""
+    p = configs.get("c4_small", n_steps=10)
+    p["fill"] = []
+    sim = dsmc_gpu.Simulation(p, debug=True)
+    sim.generate()
+    sim.step(configs.n_steps(p))
+    rc, cnt = sim.status()
+    assert rc == 0
+    for c in cnt:
+        assert c["n_store"] == 0 and c["live"] == 0 and c["candidates"] == 0 and c["max_ppc"] == 0
+    refs = [oracle_mod.OracleRun(p, r) for r in range(p["n_runs"])]
+    for o in refs:
+        o.step(configs.n_steps(p))
+    for slot in range(configs.n_slots(p)):
+        sums = sim.read_sums(slot)
+        assert not sums.any()
+        want = np.array([o.get_snap(slot) for o in refs]).transpose(1, 0, 2)
+        assert np.array_equal(sums, want)
+        m = sim.read_macros(slot)
+        assert (m[:, 0] == 0).all() and np.isnan(m[:, 1:5]).all()
+    gi = sim.get_index(0)
+    assert (gi["count"] == 0).all() and len(gi["lcr"]) == 0
