@@ -220,11 +220,13 @@ def run_ours(args):
     step_ms_sum = sum(v["ms"] for v in kern.values())
     # Interaction runs as two launches (warp tiles, then the heavy tiles they hand
     # over); the roofline treats them as one kernel with k_collide's byte count
-    cand = {k: v for k, v in kern.items() if k not in ("k_collide", "k_collide_heavy")}
+    # (sparse problems add the triage that lists the tiles with work)
+    parts = [k for k in ("k_collide_triage", "k_collide", "k_collide_heavy") if k in kern]
+    cand = {k: v for k, v in kern.items() if k not in parts}
     if "k_collide" in kern:
-        ms = kern["k_collide"]["ms"] + kern.get("k_collide_heavy", {"ms": 0.0})["ms"]
+        ms = sum(kern[k]["ms"] for k in parts)
         b = kern["k_collide"]["bytes"]
-        name = "k_collide+k_collide_heavy" if "k_collide_heavy" in kern else "k_collide"
+        name = "+".join(parts)
         cand[name] = dict(ms=ms, gbs=b / (ms / 1e3) / 1e9 if b else None, bytes=b)
     dom = max(cand, key=lambda k: cand[k]["ms"])
     d = cand[dom]
@@ -239,7 +241,7 @@ def run_ours(args):
     phases = {}
     for ph, names in (("motion+sort", ("k_zero", "k_motion", "k_scan_reduce", "k_scan_partials", "k_scan_down",
                                         "k_scatter")),
-                      ("collide+sample", ("k_collide", "k_collide_heavy"))):
+                      ("collide+sample", ("k_collide_triage", "k_collide", "k_collide_heavy"))):
         ms = sum(kern[k]["ms"] for k in names if k in kern)
         b = sum(kern[k]["bytes"] or 0 for k in names if k in kern)
         if ms > 0:

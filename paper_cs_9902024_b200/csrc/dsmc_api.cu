@@ -14,6 +14,12 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include "dsmc.h"
+
+// mean fill density (particles per cell) below which the step lists the collide tiles
+// with work first (k_collide_triage); DSMC_COMPACT=0/1 overrides it
+#ifndef DSMC_COMPACT_PPC
+#define DSMC_COMPACT_PPC 4.0
+#endif
 #include "dsmc_device.cuh"
 #include "dsmc_kernels.h"
 
@@ -51,9 +57,9 @@ struct Layout {
   int32_t n_face;
   // ctl offsets
   size_t c_maxn, c_stepslot, c_step, c_status, c_nstore, c_parity, c_reorder, c_inserted, c_counters, c_live, c_psteps, c_slot, c_queue, c_heavy,
-      c_items;
+      c_items, c_tiles;
   // scratch offsets
-  size_t s_face_j, s_face_k, s_open, s_kept, s_part, s_macros, s_heavy, s_cand, s_acc;
+  size_t s_face_j, s_face_k, s_open, s_kept, s_part, s_macros, s_heavy, s_tiles, s_cand, s_acc;
 };
 
 // face-cell lists of the x- face (reading R8)
@@ -163,6 +169,7 @@ int make_layout(const dsmc_problem* p, int debug, Layout& L) {
   L.c_queue = o; o = align_up(o + 8 * 8, 16);
   L.c_items = o; o = align_up(o + 8 * ((size_t)R + 2), 16);
   L.c_heavy = o; o = align_up(o + 4 * 2 * dsmc::HEAVY_TIERS, 16);
+  L.c_tiles = o; o = align_up(o + 4 * 2, 16);
   s.ctl = o;
   const size_t F = (size_t)p->ny * p->nz;
   o = 0;
@@ -174,6 +181,7 @@ int make_layout(const dsmc_problem* p, int debug, Layout& L) {
   L.s_part = o; o = align_up(o + 4 * ((size_t)dsmc::scan_tiles(Lscan) + 1), 256);
   L.s_macros = o; o = align_up(o + 8 * 10 * (size_t)L.Nc, 256);
   L.s_heavy = o; o = align_up(o + 4 * dsmc::HEAVY_TIERS * ((size_t)(L.RN + 31) / 32 + 1), 256);
+  L.s_tiles = o; o = align_up(o + 4 * ((size_t)(L.RN + 31) / 32 + 1), 256);
   if (debug) {
     L.s_cand = o; o = align_up(o + 8 * (size_t)L.RN, 256);
     L.s_acc = o; o = align_up(o + 4 * (size_t)L.RN, 256);
@@ -307,6 +315,9 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
     }
     const double ppc = filled / (double)L.Nc;
     P.net_wide = (ppc > 12.0 || p->inflow_kind == DSMC_INFLOW_EFFUSIVE) ? 1 : 0;
+    // sparse fills: most tiles draw no candidate; list the ones with work (k_collide_triage)
+    P.compact = ppc < DSMC_COMPACT_PPC ? 1 : 0;
+    if (const char* e = std::getenv("DSMC_COMPACT")) P.compact = std::atoi(e) ? 1 : 0;   // A/B experiments
     // warp-tile staging capacity: the densest fill region's 32 cells with a
     // wide margin (tiles beyond it take the per-lane global-memory path)
     int32_t ppc_max = 0;
@@ -374,6 +385,8 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   P.ctl.queue = (unsigned long long*)(ct + L.c_queue);
   P.ctl.items = (int64_t*)(ct + L.c_items);
   P.ctl.heavy = (uint32_t*)(ct + L.c_heavy);
+  P.ctl.tiles = (uint32_t*)(ct + L.c_tiles);
+  P.tile_list = (uint32_t*)(sc + L.s_tiles);
   P.heavy_list = (uint32_t*)(sc + L.s_heavy);
   P.heavy_stride = (L.RN + 31) / 32 + 1;
   // NEXT-1 A/B: DSMC_STATIC_CELLS=1 replaces the dynamic, size-tiered

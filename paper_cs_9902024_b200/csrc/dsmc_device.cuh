@@ -19,6 +19,7 @@ constexpr uint32_t DEAD_KEY = 0xFFFFFFFFu;
 constexpr float DEAD_X = -1.0e30f;           // x of a removed, not yet compacted slot
 constexpr int MAX_BOUNCE = 8;
 constexpr int HEAVY_TIERS = 2;               // heavy-tile queues by size (k_collide_heavy; k_collide picks 0/1)
+constexpr uint32_t HEAVY_SLACK = 3;          // words before the LCR slice in k_collide_heavy's staging (bulk-copy alignment)
 constexpr double TWO_PI = 6.283185307179586;
 
 enum { BC_SPECULAR = 0, BC_PERIODIC = 1, BC_DIFFUSE = 2, BC_OUTFLOW = 3, BC_INFLOW = 4 };
@@ -42,6 +43,7 @@ struct Ctl {
   int64_t* items;            // [R+2] work items of the particle kernels: prefix over runs, total, items per
                              //       run if all runs hold as many (else 0) -- k_items
   uint32_t* heavy;           // [2*HEAVY_TIERS] heavy-tile queues: count, next per size tier
+  uint32_t* tiles;           // [2] k_collide_triage's list of tiles with work: count, (spare)
 };
 
 struct Prm {
@@ -103,6 +105,8 @@ struct Prm {
   int32_t heavy_static;      // NEXT-1 A/B arm: one tier, tiles dealt to blocks round-robin (no queue)
   int64_t heavy_stride;      // entries per tier list (R*Nc/32 + 1)
   int32_t caph_tier[HEAVY_TIERS];   // staging capacity of each tier (the last one is caph)
+  int32_t compact;           // sparse problem: k_collide_triage lists the tiles with work for k_collide_list
+  uint32_t* tile_list;       // [R*Nc/32 + 1] that list
   int64_t* dbg_cand;         // [R*Nc]
   int32_t* dbg_acc;          // [R*Nc]
   Ctl ctl;

@@ -720,6 +720,7 @@ __device__ __forceinline__ uint32_t run_lcr_base(const Prm& P, int r) {
 __global__ void k_step_end(Prm P, int mode, int slot) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < 2 * HEAVY_TIERS) P.ctl.heavy[r] = 0;   // heavy-tile queues of k_collide
+  if (r == 0) P.ctl.tiles[0] = 0;                // k_collide_triage's tile list
   if (mode != 0) {  // explicit sample (1: snapshot, 2: added to the slot's time average)
     if (r == 0) P.ctl.slot_done[slot] = mode == 1 ? 1 : P.ctl.slot_done[slot] + 1;
     return;
@@ -1246,18 +1247,20 @@ __device__ __forceinline__ int sched_slot(const Prm& P, int mode, int32_t s, int
 // ONE: every 32-cell tile lies in one run (Nc % 32 == 0 or a single run): the
 // multi-run paths are compiled out (c4: 6336 -> 5328 SASS instructions, k_collide
 // 12.15 -> 11.59 ms at n = 256, fewer instruction-cache misses)
-template <int D, int NET, int MODEL, bool STEP, bool ONE>
-__global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, int mode_arg, int slot_arg, int capw) {
+// LIST: the tile comes from k_collide_triage's list (k_collide_list: persistent
+// blocks; the mbarrier is initialised once per block and completes one phase per
+// staged tile; the triage already took the run's largest cell count and queued
+// the heavy tiles)
+template <int D, int NET, int MODEL, bool STEP, bool ONE, bool LIST>
+__device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, const int slot_arg, const int capw,
+                                             const WarpSmem& W, uint64_t* bar, uint32_t& bar_phase,
+                                             const int64_t k0) {
   const int mode = STEP ? 0 : mode_arg;      // STEP: the kernel of dsmc_step (mode 0) only
-  extern __shared__ __align__(16) uint8_t dsm[];
-  __shared__ __align__(8) uint64_t s_bar;        // completion of the LCR slice's bulk copy (WPB == 1)
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const WarpSmem W = warp_smem(dsm + (size_t)wid * warp_smem_bytes(capw), capw);
+  const int lane = threadIdx.x & 31;
   const int64_t RN = (int64_t)P.R * P.Nc;
   const int64_t RS = (int64_t)P.R * P.stride;
   float* const P0 = P.P;
   float* const P1 = P.P + P.half;
-  const int64_t k0 = ((int64_t)blockIdx.x * WPB + wid) * 32;
   if (k0 >= RN) return;                          // whole warp leaves together
   const int64_t k = k0 + lane;
   const bool valid = k < RN;
@@ -1290,19 +1293,20 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
   const uint2 key = run_key(P, r);
   uint32_t ncand = 0, nacc = 0;
   // cell-occupancy skew: the step's largest particle count per cell, per run
-  if (one_run) {
+  if (LIST) {
+  } else if (one_run) {
     const uint32_t wmax = __reduce_max_sync(FULL, valid ? N : 0u);
     if (lane == 0 && wmax) atomicMax(P.ctl.maxn + r_first, wmax);
   } else if (valid && N) {
     atomicMax(P.ctl.maxn + r, N);
   }
-  if (cnt > (uint32_t)capw) {
+  if (!LIST && cnt > (uint32_t)capw) {
     // tile too large for the warp's shared memory: hand it to k_collide_heavy
     // (a whole block with a large staging area -- the "heap" of TLPDPR)
     // (tiered by size: the smaller the staging area, the more blocks per SM;
     // the static NEXT-1 arm puts every such tile in the large tier)
     if (lane == 0) {
-      const int q = (P.heavy_static || cnt > (uint32_t)P.caph_tier[0]) ? 1 : 0;      // HEAVY_TIERS == 2
+      const int q = (P.heavy_static || cnt + HEAVY_SLACK > (uint32_t)P.caph_tier[0]) ? 1 : 0;   // HEAVY_TIERS == 2
       P.heavy_list[(int64_t)q * P.heavy_stride + atomicAdd(P.ctl.heavy + 2 * q, 1u)] = (uint32_t)(k0 / 32);
     }
     return;
@@ -1320,9 +1324,9 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
       if (lane == 0) {
         const uint32_t s0 = S & ~3u, e0 = (E + 3u) & ~3u;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes before the async copy
-        mbar_init(&s_bar, 1u);
-        mbar_arrive_expect_tx(&s_bar, (e0 - s0) * 4u);
-        bulk_g2s(W.a, P.lcr + s0, (e0 - s0) * 4u, &s_bar);
+        if (!LIST) mbar_init(bar, 1u);
+        mbar_arrive_expect_tx(bar, (e0 - s0) * 4u);
+        bulk_g2s(W.a, P.lcr + s0, (e0 - s0) * 4u, bar);
       }
       __syncwarp();
     }
@@ -1343,13 +1347,13 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
     // (most of c5's sparse background): only the bulk copy is drained before the warp leaves
     const bool idle = mode == 0 && tot == 0 && slot < 0 && !P.debug && __all_sync(FULL, reo == 0);
     if (idle) {
-      if (cnt > 0) mbar_wait(&s_bar, 0u);
+      if (cnt > 0) { mbar_wait(bar, bar_phase); bar_phase ^= 1u; }
     } else {
     // largest segment of the warp (network width); element -> cell tags only
     // where the rank sort or the multi-run paths need them
     const uint32_t wN = __reduce_max_sync(FULL, valid ? N : 0u);
     if (valid && (wN > DSMC_NET_MAX || !one_run)) for (uint32_t i = 0; i < N; i++) W.cell[off + i] = (uint8_t)lane;
-    if (cnt > 0) mbar_wait(&s_bar, 0u);
+    if (cnt > 0) { mbar_wait(bar, bar_phase); bar_phase ^= 1u; }
     __syncwarp();
     // ---- C: network width by the warp's largest segment (warp-uniform)
     if (wN <= DSMC_NET_MAX) {
@@ -1560,6 +1564,119 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
   }
 }
 
+template <int D, int NET, int MODEL, bool STEP, bool ONE>
+__global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, int mode_arg, int slot_arg, int capw) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ __align__(8) uint64_t s_bar;        // completion of the LCR slice's bulk copy (WPB == 1)
+  const int wid = threadIdx.x >> 5;
+  const WarpSmem W = warp_smem(dsm + (size_t)wid * warp_smem_bytes(capw), capw);
+  uint32_t ph = 0;
+  collide_tile<D, NET, MODEL, STEP, ONE, false>(P, mode_arg, slot_arg, capw, W, &s_bar, ph,
+                                                ((int64_t)blockIdx.x * WPB + wid) * 32);
+}
+
+// Sparse problems (mean fill below DSMC_COMPACT_PPC particles per cell: c5's background,
+// c2): most tiles draw no candidate, and on a step without Sampling or reorder such a
+// tile changes nothing, but a one-warp block per tile still pays its launch and two
+// dependent global round trips (524288 blocks of c5 launch in 0.27 ms on their own).
+// k_collide_triage draws the candidate counts of R12 with one thread per cell -- the
+// same draws E0 repeats -- at full occupancy, queues the heavy tiles as k_collide would,
+// and lists the tiles with work; persistent k_collide_list blocks then take the list.
+constexpr int TRIAGE_T = 1024;
+constexpr int TRIAGE_TPW = 4;    // tiles per warp: 128 tiles per block, one list atomic per block
+template <bool ONE>
+__global__ void __launch_bounds__(TRIAGE_T) k_collide_triage(Prm P, int capw) {
+  __shared__ uint32_t s_cls[TRIAGE_T / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t RN = (int64_t)P.R * P.Nc;
+  const int32_t s = *P.ctl.step;
+  const bool all = *P.ctl.step_slot >= 0 || P.debug;     // Sampling (or debug): every tile has work
+  uint32_t cls = 0;                // 2 bits per tile of this warp: 0 idle, 1 warp list, 2 / 3 heavy tier 0 / 1
+#pragma unroll
+  for (int t = 0; t < TRIAGE_TPW; t++) {
+    const int64_t k0 = (((int64_t)blockIdx.x * (TRIAGE_T / 32) + wid) * TRIAGE_TPW + t) * 32;
+    if (k0 >= RN) break;
+    const int64_t k = k0 + lane;
+    const bool valid = k < RN;
+    const int64_t klast = k0 + 31 < RN ? k0 + 31 : RN - 1;
+    const int last_lane = (int)(klast - k0);
+    const int r_first = (int)run_of(P, (uint32_t)k0);
+    const int r_last = (int)run_of(P, (uint32_t)klast);
+    const bool one_run = ONE || r_first == r_last;
+    const uint32_t en = valid ? P.cell[k] : 0u;
+    uint32_t st = __shfl_up_sync(FULL, en, 1);
+    if (lane == 0) st = k == 0 ? 0u : P.cell[k - 1];
+    const int r = ONE ? r_first : (valid ? (int)run_of(P, (uint32_t)k) : r_last);
+    const uint32_t c = valid ? (uint32_t)k - (uint32_t)r * (uint32_t)P.Nc : 0u;
+    const uint32_t N = valid ? en - st : 0u;
+    const uint32_t S = __shfl_sync(FULL, st, 0);
+    const uint32_t E = __shfl_sync(FULL, en, last_lane);
+    // (read first: the run's maximum settles within a few tiles, and thousands of
+    // atomics per microsecond on one address would serialise)
+    if (one_run) {
+      const uint32_t wmax = __reduce_max_sync(FULL, N);
+      if (lane == 0 && wmax > P.ctl.maxn[r_first]) atomicMax(P.ctl.maxn + r_first, wmax);
+    } else if (N > P.ctl.maxn[r]) {
+      atomicMax(P.ctl.maxn + r, N);
+    }
+    uint32_t ct;
+    if (E - S > (uint32_t)capw) {
+      ct = (P.heavy_static || E - S + HEAVY_SLACK > (uint32_t)P.caph_tier[0]) ? 3u : 2u;   // HEAVY_TIERS == 2
+    } else {
+      const float gm = valid ? P.gmax[k] : 0.0f;
+      const uint32_t M = valid ? ntc_count(P, run_key(P, r), c, (uint32_t)s, N, gm) : 0u;
+      ct = (all || __any_sync(FULL, M != 0u || P.ctl.reorder[r] != 0)) ? 1u : 0u;
+    }
+    cls |= ct << (2 * t);
+  }
+  if (lane == 0) s_cls[wid] = cls;
+  __syncthreads();
+  if (wid == 0) {
+    // the block's 128 tiles in order (warp w holds 4w .. 4w+3): one atomic per list
+    const uint32_t a = s_cls[lane];
+    const uint32_t t0 = (blockIdx.x * (TRIAGE_T / 32) + lane) * TRIAGE_TPW;
+#pragma unroll
+    for (uint32_t q = 1; q <= 3; q++) {
+      uint32_t mine = 0;
+#pragma unroll
+      for (int t = 0; t < TRIAGE_TPW; t++) mine |= ((a >> (2 * t)) & 3u) == q ? 1u << t : 0u;
+      const uint32_t n = __popc(mine);
+      uint32_t pre = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(FULL, pre, o); if (lane >= o) pre += y; }
+      const uint32_t tot = __shfl_sync(FULL, pre, 31);
+      if (tot == 0) continue;
+      pre -= n;
+      uint32_t* const cnt = q == 1 ? P.ctl.tiles : P.ctl.heavy + 2 * (q - 2);
+      uint32_t* const lst = q == 1 ? P.tile_list : P.heavy_list + (int64_t)(q - 2) * P.heavy_stride;
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(cnt, tot);
+      base = __shfl_sync(FULL, base, 0) + pre;
+#pragma unroll
+      for (int t = 0; t < TRIAGE_TPW; t++)
+        if (mine & (1u << t)) lst[base + __popc(mine & ((1u << t) - 1u))] = t0 + t;
+    }
+  }
+}
+
+template <int D, int NET, int MODEL, bool ONE>
+__global__ void __launch_bounds__(32, DSMC_COLLIDE_MINB) k_collide_list(Prm P, int capw) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ __align__(8) uint64_t s_bar;
+  const WarpSmem W = warp_smem(dsm, capw);
+  if (threadIdx.x == 0) mbar_init(&s_bar, 1u);
+  __syncwarp();
+  uint32_t ph = 0;
+  const uint32_t n = *P.ctl.tiles;
+  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+    collide_tile<D, NET, MODEL, true, ONE, true>(P, 0, -1, capw, W, &s_bar, ph, (int64_t)P.tile_list[i] * 32);
+    // every lane's generic shared-memory accesses of this tile are ordered before the
+    // next tile's bulk copy (async proxy) overwrites the staging area
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // k_collide_heavy: the warp tiles k_collide could not stage (dense cells, e.g.
 // c5's orifice jet).  The GPU analog of TLPDPR's processor heap (PAPER.md
@@ -1664,10 +1781,16 @@ __global__ void __launch_bounds__(HT) k_collide_heavy(Prm P, int mode, int slot_
     while (c_st[last] == 0xFFFFFFFFu) last--;
     const uint32_t S = c_st[0], E = c_st[last] + c_N[last], cnt = E - S;
     if (t == 32) c_st[32] = E;
+    // every thread's generic accesses of the previous tile's staging ordered before
+    // this tile's bulk copy (async proxy) overwrites it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     const float gm0 = gm;
     uint32_t ncand = 0, nacc = 0;
-    if (cnt <= (uint32_t)caph) {
+    // the bulk copy's 16-byte aligned window puts the slice at offset S & 3 (<= 3 words)
+    // of the staging buffer: the slice itself must fit, or its last words would land
+    // in the buffer C's chunk sort writes while other warps still read them
+    if (cnt + HEAVY_SLACK <= (uint32_t)caph) {
       // ---- B: the tile's LCR slice is contiguous: one thread moves its 16-byte aligned
       // window into shared memory with a bulk copy on an mbarrier while the block tags
       // every element with its cell.  It lands in the buffer the chunk sort of C does
@@ -2201,6 +2324,63 @@ static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t s
   k_collide<D, NET, MODEL, STEP, ONE><<<g, WPB * 32, smem, st>>>(P, mode, slot, capw);
 }
 
+template <int D, int NET, int MODEL, bool ONE>
+static void collide_list_t(const Prm& P, int capw, cudaStream_t st) {
+  const size_t smem = warp_smem_bytes(capw);
+  static size_t configured_dev[MAX_DEV] = {0};
+  static int occ_dev[MAX_DEV] = {0};
+  const int dev = cur_dev();
+  if (smem > configured_dev[dev]) {
+    cudaFuncSetAttribute(k_collide_list<D, NET, MODEL, ONE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured_dev[dev] = smem;
+    occ_dev[dev] = 0;
+  }
+  int& occ = occ_dev[dev];
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collide_list<D, NET, MODEL, ONE>, 32, smem);
+    if (occ < 1) occ = 1;
+  }
+  const int64_t tiles = ((int64_t)P.R * P.Nc + 31) / 32;
+  int64_t g = (int64_t)num_sms() * occ;
+  if (g > tiles) g = tiles;
+  k_collide_list<D, NET, MODEL, ONE><<<(unsigned)g, 32, smem, st>>>(P, capw);
+}
+
+template <int D, int NET>
+static void collide_list_m(const Prm& P, cudaStream_t st) {
+  const bool one = P.Nc % 32 == 0 || P.R == 1;
+  if (P.model == DSMC_MODEL_HS) {
+    if (one) collide_list_t<D, NET, DSMC_MODEL_HS, true>(P, P.capw, st);
+    else collide_list_t<D, NET, DSMC_MODEL_HS, false>(P, P.capw, st);
+  } else {
+    if (one) collide_list_t<D, NET, DSMC_MODEL_VHS, true>(P, P.capw, st);
+    else collide_list_t<D, NET, DSMC_MODEL_VHS, false>(P, P.capw, st);
+  }
+}
+
+// sparse problems: the tiles with work listed by k_collide_triage, then collided
+// by persistent k_collide_list blocks (mode 0 only)
+static void launch_collide_compact(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
+  const int64_t tiles = ((int64_t)P.R * P.Nc + 31) / 32;
+  const bool one = P.Nc % 32 == 0 || P.R == 1;
+  const int64_t per_block = TRIAGE_T / 32 * TRIAGE_TPW;
+  const unsigned g = (unsigned)((tiles + per_block - 1) / per_block);
+  hook.before(KSLOT_COLLIDE_TRIAGE);
+  if (one) k_collide_triage<true><<<g, TRIAGE_T, 0, st>>>(P, P.capw);
+  else k_collide_triage<false><<<g, TRIAGE_T, 0, st>>>(P, P.capw);
+  hook.after(KSLOT_COLLIDE_TRIAGE);
+  hook.before(KSLOT_COLLIDE);
+  const bool wide = P.net_wide != 0;
+  if (P.dim == 1) {
+    if (wide) collide_list_m<1, 32>(P, st); else collide_list_m<1, 16>(P, st);
+  } else if (P.dim == 2) {
+    if (wide) collide_list_m<2, 32>(P, st); else collide_list_m<2, 16>(P, st);
+  } else {
+    if (wide) collide_list_m<3, 32>(P, st); else collide_list_m<3, 16>(P, st);
+  }
+  hook.after(KSLOT_COLLIDE);
+}
+
 template <int D, int NET>
 static void collide_m(const Prm& P, int mode, int slot, int capw, cudaStream_t st) {
   if (mode == 0) {
@@ -2299,9 +2479,13 @@ void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
   hook.before(KSLOT_SCATTER);
   launch_scatter(P, st);
   hook.after(KSLOT_SCATTER);
-  hook.before(KSLOT_COLLIDE);
-  launch_collide(P, 0, -1, st);
-  hook.after(KSLOT_COLLIDE);
+  if (P.compact) {
+    launch_collide_compact(P, st, hook);
+  } else {
+    hook.before(KSLOT_COLLIDE);
+    launch_collide(P, 0, -1, st);
+    hook.after(KSLOT_COLLIDE);
+  }
   hook.before(KSLOT_COLLIDE_HEAVY);
   launch_collide_heavy(P, 0, -1, st);
   hook.after(KSLOT_COLLIDE_HEAVY);
@@ -2336,6 +2520,7 @@ const char* kernel_slot_name(int k) {
     case KSLOT_SCATTER: return "k_scatter";
     case KSLOT_COLLIDE: return "k_collide";
     case KSLOT_COLLIDE_HEAVY: return "k_collide_heavy";
+    case KSLOT_COLLIDE_TRIAGE: return "k_collide_triage";
     case KSLOT_STEP_END: return "k_step_end";
     default: return "";
   }

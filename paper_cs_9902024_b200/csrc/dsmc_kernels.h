@@ -20,6 +20,7 @@ enum KernelSlot {
   KSLOT_COLLIDE,
   KSLOT_STEP_END,
   KSLOT_COLLIDE_HEAVY,
+  KSLOT_COLLIDE_TRIAGE,
   KSLOT_COUNT
 };
 

@@ -144,6 +144,46 @@ def test_one_step_parity_heavy_chunk_edges(dsmc_gpu, oracle_mod):
     one_step_case(dsmc_gpu, oracle_mod, p, 0, 2, seed_state=st)
 
 
+def test_one_step_parity_heavy_tier_edge(dsmc_gpu, oracle_mod):
+    """Tiles at the small heavy tier's capacity (3584) whose LCR slice starts at
+    S & 3 = 1..3: the bulk copy's aligned window then needs up to 3 more words than
+    the tile holds (HEAVY_SLACK), so such tiles must take the large tier.  (Staged
+    in the small tier, the slice's last words overlapped the chunk sort's output and
+    the result depended on warp timing.)"""
+    p = configs.get("c4_small")
+    p["reorder_every"] = 1
+    p["fill"] = []
+    parts, seed = [], 30
+    # cell 32 (tile 1) holds 3 particles, so tile 2 starts at S = 3; then tiles of
+    # 3584, 3583, 3582, 3581 particles put S & 3 at 3, 2, 0, 1
+    parts.append(inputs.clustered_state(seed, p, [32], 3))
+    for t, n in zip((2, 3, 4, 5), (3584, 3583, 3582, 3581)):
+        per = [n // 32 + (1 if c < n % 32 else 0) for c in range(32)]
+        for c, m in enumerate(per):
+            seed += 1
+            parts.append(inputs.clustered_state(seed, p, [32 * t + c], m))
+    st = {k: np.concatenate([q[k] for q in parts]) for k in parts[0]}
+    p["cap_per_run"] = len(st["x"]) + 64
+    for s0 in (2, 3, 4):
+        one_step_case(dsmc_gpu, oracle_mod, p, 0, s0, seed_state=st)
+
+
+def test_repeatable_developed_jet(dsmc_gpu):
+    """The same problem run twice gives the same bits (R4: a run is a function of its
+    key), here through c5's developed jet, whose dense tiles exercise both heavy tiers
+    and their bulk-copy staging for hundreds of steps.  (A staging race at the small
+    tier's capacity once made this diverge after ~250 steps.)"""
+    def run():
+        p = configs.get("c5", n_runs=2, n_steps=400, cap_per_run=12 << 20)
+        sim = dsmc_gpu.Simulation(p)
+        sim.generate()
+        sim.step(320)
+        return sim.get_state(1)
+    a, b = run(), run()
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+
+
 def test_one_step_parity_giant_cell(dsmc_gpu, oracle_mod):
     """A cell beyond even the heavy staging area (9000 > 8192 particles):
     the per-thread global-memory fallback of k_collide_heavy."""
@@ -552,6 +592,31 @@ def test_staging_capacity_does_not_change_results(dsmc_gpu, monkeypatch, name, s
             sa, sb = sim.get_state(r), ref.get_state(r)
             for k in sa:
                 assert np.array_equal(sa[k], sb[k]), (capw, r, k)
+
+
+@pytest.mark.parametrize("name,steps,n_runs", [("c2_small", 12, None), ("c5_small", 30, None), ("c4_small", 7, None),
+                                               ("c5", 60, 2)])
+def test_tile_list_equals_full_grid(dsmc_gpu, monkeypatch, name, steps, n_runs):
+    """Sparse problems list the collide tiles with work first (k_collide_triage, then
+    persistent k_collide_list blocks): with the list forced on or off
+    (DSMC_COMPACT) the states, majorants and counters are bit-identical, over reorder
+    and Sampling steps."""
+    def run(compact):
+        monkeypatch.setenv("DSMC_COMPACT", str(compact))
+        p = configs.get(name) if n_runs is None else configs.get(name, n_runs=n_runs)
+        sim = dsmc_gpu.Simulation(p)
+        sim.generate()
+        sim.step(steps)
+        return sim, p
+    a, p = run(1)
+    b, _ = run(0)
+    assert a.status()[1] == b.status()[1]
+    for r in range(p["n_runs"]):
+        sa, sb = a.get_state(r), b.get_state(r)
+        for k in sa:
+            assert np.array_equal(sa[k], sb[k]), (r, k)
+        assert np.array_equal(a.get_gmax(r), b.get_gmax(r)), r
+    assert "k_collide_triage" in a.step_timed(1) and "k_collide_triage" not in b.step_timed(1)
 
 
 @pytest.mark.parametrize("nan_pos", [3, 4000, None])

@@ -46,7 +46,7 @@ for name, (ms, cnt) in timed.items():
     out["kernels"][name] = {"ms": round(m, 4), "GB/s": round(b / (m / 1e3) / 1e9, 1) if b else None}
     if name in ("k_zero", "k_motion", "k_scan_reduce", "k_scan_partials", "k_scan_down", "k_scatter"):
         ph["motion+sort"][0] += m; ph["motion+sort"][1] += b
-    if name in ("k_collide", "k_collide_heavy"):
+    if name in ("k_collide_triage", "k_collide", "k_collide_heavy"):
         ph["collide+sample"][0] += m; ph["collide+sample"][1] += b
 out["phases"] = {k: {"ms": round(v[0], 4), "frac_measured": round(v[1] / (v[0] / 1e3) / 1e9 / hbm, 4),
                      "frac_8TBs": round(v[1] / (v[0] / 1e3) / 1e9 / 8000, 4)} for k, v in ph.items()}

@@ -24,7 +24,7 @@ for n, v in seq:
     a[0] += 1
     a[1] += v
 step_kernels = {"k_zero", "k_motion", "k_step_mid", "k_scan_reduce", "k_scan_partials", "k_scan_down", "k_scatter",
-                "k_collide", "k_step_end", "k_inflow_count", "k_inflow_emit"}
+                "k_collide", "k_collide_list", "k_collide_triage", "k_step_end", "k_inflow_count", "k_inflow_emit"}
 step_total = sum(v[1] for n, v in agg.items() if n in step_kernels)
 lines.append(f"# {tag} profile summary — {cfg}\n")
 lines.append(f"Launch list: `{os.path.basename(launch_csv)}` (ncu `--metrics gpu__time_duration.sum "
