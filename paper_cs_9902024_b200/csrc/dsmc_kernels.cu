@@ -852,6 +852,30 @@ __device__ __forceinline__ void pair_of(uint32_t w, uint32_t N, uint32_t& i, uin
 #ifndef DSMC_CCW
 #define DSMC_CCW 128        // pre-drawn candidates per pass of k_collide's E1
 #endif
+#ifndef DSMC_LANE_UNROLL_N
+#define DSMC_LANE_UNROLL_N 1   // unroll of k_collide's lane-strided gather / write-back loops (A/B; see below)
+#endif
+#define DSMC_PRAGMA(x) _Pragma(#x)
+#define DSMC_PRAGMA_UNROLL(n) DSMC_PRAGMA(unroll n)
+#ifdef DSMC_LANE_UNROLL_NONE
+#define DSMC_LANE_UNROLL
+#else
+#define DSMC_LANE_UNROLL DSMC_PRAGMA_UNROLL(DSMC_LANE_UNROLL_N)
+#endif
+// Loop unrolling in k_collide, measured at c4 n = 256 (k_collide ms): the compiler's own
+// unrolling of the lane-strided gather / write-back loops 11.46, kept rolled 10.10 (2x:
+// 10.35, 4x: 10.62) -- the unrolled copies cost more in code size and registers than the
+// loop overhead they save; the candidate walk rolled as well 10.02 (compiler: 10.10, 4x:
+// 10.73); the other runtime-trip loops (E1 passes, Sampling, rank sort) rolled: 10.06-10.07,
+// left to the compiler: 10.02.
+#ifdef DSMC_LOOP_UNROLL_ONE         // A/B: the other runtime-trip loops rolled
+#define DSMC_LOOP_UNROLL DSMC_PRAGMA_UNROLL(1)
+#else
+#define DSMC_LOOP_UNROLL
+#endif
+#ifndef DSMC_WALK_UNROLL_N
+#define DSMC_WALK_UNROLL_N 1   // 0: the compiler's choice
+#endif
 struct SmemCell4 {          // shared-memory cell, velocities as float4 (x, y, z, -): one LDS.128 / STS.128
   float4* v;
   __device__ void ld(uint32_t i, float a[3]) const { const float4 t = v[i]; a[0] = t.x; a[1] = t.y; a[2] = t.z; }
@@ -974,6 +998,9 @@ __device__ __noinline__ void marsaglia_pq_from(uint2 key, uint32_t c, uint32_t s
 template <int MODEL, class A>
 __device__ __forceinline__ void ntc_apply_pre(const Prm& P, const A& acc, double gm, const uint32_t* ij,
                                               const float4* rec, uint32_t n, float& maxg2, uint32_t& nacc) {
+#if DSMC_WALK_UNROLL_N > 0
+  DSMC_PRAGMA_UNROLL(DSMC_WALK_UNROLL_N)
+#endif
   for (uint32_t k = 0; k < n; k++) {
     const uint32_t pr = ij[k];
     const uint32_t i = pr & 0xFFFFu, j = pr >> 16;
@@ -1042,6 +1069,7 @@ template <class A>
 __device__ __forceinline__ void sample_cell(const Prm& P, int slot, int64_t k, uint32_t N, const A& acc,
                                             bool add = false) {
   double sx = 0.0, sy = 0.0, sz = 0.0, se = 0.0;
+  DSMC_LOOP_UNROLL
   for (uint32_t i = 0; i < N; i++) {
     float a[3];
     acc.ld(i, a);
@@ -1143,6 +1171,7 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
                                             uint2 key_u) {
     const unsigned lt = (1u << lane) - 1u;
     uint32_t nfail = 0;        // candidates whose first Marsaglia try (pair block) was rejected
+    DSMC_LOOP_UNROLL
     for (uint32_t q0 = 0; q0 < lim; q0 += 64) {
       uint32_t qq[2], kq[2], nc[2];
       double gq_hat[2];
@@ -1204,6 +1233,7 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
     }
     // rejected first tries (about one candidate in five), compacted: direction blocks
     __syncwarp();
+    DSMC_LOOP_UNROLL
     for (uint32_t f0 = 0; f0 < nfail; f0 += 32) {
       const bool act = f0 + lane < nfail;
       const uint32_t q = act ? W.fl[f0 + lane] : 0u;
@@ -1373,6 +1403,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
       }
     } else {
       if (valid && N <= (uint32_t)NET) sort_segment<NET, NET>(wa + off, W.sorted + off, N);
+      DSMC_LOOP_UNROLL
       for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
         const uint32_t q = q0 + lane;
         const int cq = q < cnt ? W.cell[q] : 0;
@@ -1380,6 +1411,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
         if (q < cnt && n > (uint32_t)NET) {
           const uint32_t v = wa[q];
           uint32_t rank = 0;
+          DSMC_LOOP_UNROLL
           for (uint32_t p = 0; p < n; p++) rank += wa[b + p] < v ? 1u : 0u;
           W.sorted[b + rank] = v;
         }
@@ -1396,6 +1428,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
       // velocities in canonical order: 4-byte cp.async gathers straight into shared
       // memory (no registers held while they are in flight); they complete while
       // E1 draws the candidates, and the walk E2 waits for them
+      DSMC_LANE_UNROLL
       for (uint32_t q = lane; q < cnt; q += 32) {
         const uint32_t g = W.sorted[q];
         float* d = reinterpret_cast<float*>(v4 + q);
@@ -1406,6 +1439,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
       cp_async_commit();
       // (on reorder steps the positions move in F, once the staging arrays are free)
     } else {
+      DSMC_LOOP_UNROLL
       for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
         const uint32_t q = q0 + lane;
         const int cq = q < cnt ? W.cell[q] : 0;
@@ -1433,6 +1467,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
       SmemCell4 Au{v4 + off};
       float maxg2 = 0.0f;
       uint32_t naccu = 0;
+      DSMC_LOOP_UNROLL
       for (uint32_t base = 0; base < tot; base += CCW) {
         const uint32_t lim = tot - base < (uint32_t)CCW ? tot - base : (uint32_t)CCW;
         // two candidates per lane per pass: four independent Philox chains in flight
@@ -1473,6 +1508,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
         float* __restrict__ dx = (h ? P0 : P1) + (int64_t)r * P.stride + (S - rbase);
         float* __restrict__ dy = dx + RS;
         float* __restrict__ dz = dy + RS;
+        DSMC_LANE_UNROLL
         for (uint32_t q = lane; q < cnt; q += 32) {
           const float4 v = v4[q];
           dx[3 * RS + q] = v.x;
@@ -1483,6 +1519,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
         const float* __restrict__ px = (h ? P1 : P0);
         const float* __restrict__ py = px + RS;
         const float* __restrict__ pz = py + RS;
+        DSMC_LANE_UNROLL
         for (uint32_t q = lane; q < cnt; q += 32) {
           const uint32_t g = W.sorted[q];
           float* d = reinterpret_cast<float*>(v4 + q);
@@ -1493,6 +1530,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
         cp_async_commit();
         cp_async_wait_all();
         __syncwarp();
+        DSMC_LANE_UNROLL
         for (uint32_t q = lane; q < cnt; q += 32) {
           const float4 v = v4[q];
           dx[q] = v.x;
@@ -1503,6 +1541,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
         float* __restrict__ vxp = (h ? P1 : P0) + 3 * RS;
         float* __restrict__ vyp = vxp + RS;
         float* __restrict__ vzp = vyp + RS;
+        DSMC_LANE_UNROLL
         for (uint32_t q = lane; q < cnt; q += 32) {
           const uint32_t g = W.sorted[q];
           const float4 v = v4[q];
@@ -1512,6 +1551,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
         }
       }
     } else {
+      DSMC_LOOP_UNROLL
       for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
         const uint32_t q = q0 + lane;
         const int cq = q < cnt ? W.cell[q] : 0;
