@@ -1,5 +1,5 @@
 """Write profiles/<tag>_*.md/json summaries from gpurun_out ncu artefacts.
-usage: python tools/summarize_profiles.py TAG LAUNCH_CSV NCU_REP CONFIG"""
+usage: python tools/summarize_profiles.py TAG LAUNCH_CSV NCU_REP_OR_RAW_CSV_GZ CONFIG"""
 import csv
 import io
 import json
@@ -35,7 +35,11 @@ for n, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
     share = f"{100 * t / step_total:.1f}%" if n in step_kernels else "(setup)"
     lines.append(f"| {n} | {c} | {t / c / 1e3:.1f} | {share} |")
 # ---- full metrics
-out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if rep.endswith(".csv.gz"):       # exported on the GPU box by tools/ncu_export.sh
+    import gzip
+    out = gzip.open(rep, "rt").read()
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(io.StringIO(out)))
 h, u = rr[0], rr[1]
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
