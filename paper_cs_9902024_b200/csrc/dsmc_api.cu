@@ -229,6 +229,8 @@ struct dsmc_ctx {
   int debug;
   cudaStream_t stream;
   cudaStream_t cap_stream;
+  cudaStream_t aux_stream;   // the graph's second branch (heavy tiles beside the warp-tile list)
+  cudaEvent_t fork, join;
   cudaGraph_t graph;
   cudaGraphExec_t exec;
   int kernels_per_step;
@@ -402,6 +404,9 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
     if (c->exec) cudaGraphExecDestroy(c->exec);
     if (c->graph) cudaGraphDestroy(c->graph);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+    if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+    if (c->fork) cudaEventDestroy(c->fork);
+    if (c->join) cudaEventDestroy(c->join);
     delete c;
     return code;
   };
@@ -409,7 +414,10 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   std::vector<uint8_t> open;
   face_lists(p, fj, fk, open);
   cudaError_t e;
-  if ((e = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking)) != cudaSuccess)
+  if ((e = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming)) != cudaSuccess)
     return bail(cuda_fail(e, "cudaStreamCreate"));
   if (!fj.empty()) {
     cudaMemcpyAsync((void*)P.face_j, fj.data(), 4 * fj.size(), cudaMemcpyHostToDevice, c->stream);
@@ -427,7 +435,7 @@ int dsmc_create(const dsmc_problem* prob, const dsmc_buffers* buf, int32_t debug
   // capture one step as a graph (device-side schedule: one graph for all steps)
   if ((e = cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
     return bail(cuda_fail(e, "cudaStreamBeginCapture"));
-  dsmc::issue_step(P, c->cap_stream, dsmc::LaunchHook{});
+  dsmc::issue_step(P, c->cap_stream, dsmc::LaunchHook{}, dsmc::Branch{c->aux_stream, c->fork, c->join});
   if ((e = cudaStreamEndCapture(c->cap_stream, &c->graph)) != cudaSuccess) {
     c->graph = nullptr;
     return bail(cuda_fail(e, "cudaStreamEndCapture"));
@@ -455,6 +463,9 @@ int dsmc_destroy(dsmc_ctx* c) {
   if (c->exec) cudaGraphExecDestroy(c->exec);
   if (c->graph) cudaGraphDestroy(c->graph);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+  if (c->fork) cudaEventDestroy(c->fork);
+  if (c->join) cudaEventDestroy(c->join);
   delete c;
   return DSMC_OK;
 }

@@ -2400,7 +2400,9 @@ static void collide_list_m(const Prm& P, cudaStream_t st) {
 
 // sparse problems: the tiles with work listed by k_collide_triage, then collided
 // by persistent k_collide_list blocks (mode 0 only)
-static void launch_collide_compact(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
+void launch_collide_heavy(const Prm& P, int mode, int slot, cudaStream_t st);
+
+static void launch_collide_compact(const Prm& P, cudaStream_t st, const LaunchHook& hook, const Branch& br) {
   const int64_t tiles = ((int64_t)P.R * P.Nc + 31) / 32;
   const bool one = P.Nc % 32 == 0 || P.R == 1;
   const int64_t per_block = TRIAGE_T / 32 * TRIAGE_TPW;
@@ -2409,6 +2411,14 @@ static void launch_collide_compact(const Prm& P, cudaStream_t st, const LaunchHo
   if (one) k_collide_triage<true><<<g, TRIAGE_T, 0, st>>>(P, P.capw);
   else k_collide_triage<false><<<g, TRIAGE_T, 0, st>>>(P, P.capw);
   hook.after(KSLOT_COLLIDE_TRIAGE);
+  // the triage queued the heavy tiles: with a second branch they run beside the
+  // warp-tile list (the tiers' persistent blocks fill SMs the list's tail leaves idle)
+  if (br.st) {
+    cudaEventRecord(br.fork, st);
+    cudaStreamWaitEvent(br.st, br.fork, 0);
+    launch_collide_heavy(P, 0, -1, br.st);
+    cudaEventRecord(br.join, br.st);
+  }
   hook.before(KSLOT_COLLIDE);
   const bool wide = P.net_wide != 0;
   if (P.dim == 1) {
@@ -2502,7 +2512,8 @@ void launch_selftest_philox(int64_t n, const uint32_t* ctr, uint32_t k0, uint32_
 }
 
 // one full step: kernel order of PAPER.md Fig. 1
-void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
+void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook, const Branch& br_in) {
+  const Branch br = (P.compact && !hook.fn && !std::getenv("DSMC_NO_BRANCH")) ? br_in : Branch{};
   hook.before(KSLOT_ZERO);
   launch_zero(P.cell, (int64_t)P.R * P.Nc, st);
   hook.after(KSLOT_ZERO);
@@ -2520,15 +2531,19 @@ void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook) {
   launch_scatter(P, st);
   hook.after(KSLOT_SCATTER);
   if (P.compact) {
-    launch_collide_compact(P, st, hook);
+    launch_collide_compact(P, st, hook, br);
   } else {
     hook.before(KSLOT_COLLIDE);
     launch_collide(P, 0, -1, st);
     hook.after(KSLOT_COLLIDE);
   }
-  hook.before(KSLOT_COLLIDE_HEAVY);
-  launch_collide_heavy(P, 0, -1, st);
-  hook.after(KSLOT_COLLIDE_HEAVY);
+  if (br.st) {
+    cudaStreamWaitEvent(st, br.join, 0);
+  } else {
+    hook.before(KSLOT_COLLIDE_HEAVY);
+    launch_collide_heavy(P, 0, -1, st);
+    hook.after(KSLOT_COLLIDE_HEAVY);
+  }
   hook.before(KSLOT_STEP_END);
   launch_step_end(P, 0, 0, st);
   hook.after(KSLOT_STEP_END);

@@ -40,7 +40,13 @@ void launch_fill(const Prm& P, cudaStream_t st);
 void launch_macros(const Prm& P, const double* sums, int n_blocks, int m, double fnum_vc, cudaStream_t st);
 void launch_selftest_philox(int64_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out,
                             uint32_t* out_ref, cudaStream_t st);
-void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook);
+// an optional second branch for graph capture: the heavy tiles of a triaged (sparse)
+// step run on `st` forked from and joined back into the main stream by the two events
+struct Branch {
+  cudaStream_t st = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+void issue_step(const Prm& P, cudaStream_t st, const LaunchHook& hook, const Branch& br = Branch{});
 void issue_sample(const Prm& P, int slot, int add, cudaStream_t st);
 const char* kernel_slot_name(int k);
 
