@@ -17,8 +17,9 @@
  *   - Device buffers are allocated and owned by the CALLER (the Python binding
  *     uses torch), sized by dsmc_query_sizes(); the library borrows them from
  *     dsmc_create() until dsmc_destroy() and allocates no device memory on the
- *     DSMC path.  A context owns its CUDA graph (and graph exec) and a capture
- *     stream, released by dsmc_destroy.  The one exception is the test hook
+ *     DSMC path.  A context owns its CUDA graph (and graph exec), a capture
+ *     stream, a second stream and two events for the graph's heavy-tile branch,
+ *     released by dsmc_destroy.  The one exception is the test hook
  *     dsmc_selftest_philox, which allocates and frees its own scratch buffers.
  *   - All calls are asynchronous on the caller's CUDA stream except those
  *     marked SYNC, which synchronise that stream.  Device-side faults
@@ -35,7 +36,9 @@
  *     bit-identical with or without them): DSMC_STATIC_CELLS=1 disables the
  *     heavy-tile queue (static lane-per-cell mapping, NEXT-1); DSMC_CAPW=<n>
  *     overrides the warp-tile staging capacity; DSMC_CARVEOUT=<percent> sets the
- *     collide kernel's preferred shared-memory carveout.
+ *     collide kernel's preferred shared-memory carveout; DSMC_COMPACT=0/1 forces
+ *     the sparse-problem tile list (k_collide_triage) off or on; DSMC_NO_BRANCH=1
+ *     keeps the heavy tiers on the main stream of the graph.
  */
 #ifndef DSMC_H
 #define DSMC_H
