@@ -873,6 +873,9 @@ __device__ __forceinline__ void pair_of(uint32_t w, uint32_t N, uint32_t& i, uin
 #else
 #define DSMC_LOOP_UNROLL
 #endif
+#ifndef DSMC_OWNMAP
+#define DSMC_OWNMAP 1          // E1 finds a candidate's cell in a byte map instead of a search (A/B)
+#endif
 #ifndef DSMC_WALK_UNROLL_N
 #define DSMC_WALK_UNROLL_N 1   // 0: the compiler's choice
 #endif
@@ -1141,12 +1144,13 @@ struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
   float4* rec;              // [CCW] pre-drawn candidate: unit vector (R14) and acceptance threshold / word
   uint32_t* cij;            // [CCW] candidate pair i | j << 16
   uint8_t* cell; uint8_t* fl;
+  uint8_t* own;             // [CCW] owning cell (lane) of each candidate of the E1 pass (DSMC_OWNMAP)
 };
 
 // the staged LCR slice `a` (the bulk copy's 16-byte aligned window around [S, E): up
 // to 3 words of slack on either side) aliases the 16 capw bytes of v4
 __host__ __device__ inline size_t warp_smem_bytes(int capw) {   // capw a multiple of 32
-  return (size_t)capw * (4 + 16 + 1) + (size_t)CCW * (16 + 4 + 1) + 16;
+  return (size_t)capw * (4 + 16 + 1) + (size_t)CCW * (16 + 4 + 1 + (DSMC_OWNMAP ? 1 : 0)) + 16;
 }
 
 __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
@@ -1158,6 +1162,7 @@ __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
   w.cij = reinterpret_cast<uint32_t*>(w.rec + CCW);
   w.cell = reinterpret_cast<uint8_t*>(w.cij + CCW);
   w.fl = w.cell + capw;      // candidates whose first Marsaglia try was rejected
+  w.own = w.fl + CCW;
   return w;
 }
 
@@ -1167,10 +1172,21 @@ __device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
 // lies in one run, whose key key_u is then warp-uniform.
 template <bool UK, int MODEL>
 __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int lane, uint32_t base, uint32_t lim,
-                                            uint32_t mst, uint32_t N, double ghatu, int r, uint32_t c, uint32_t s,
-                                            uint2 key_u) {
+                                            uint32_t mst, uint32_t M, uint32_t N, double ghatu, int r, uint32_t c,
+                                            uint32_t s, uint2 key_u) {
     const unsigned lt = (1u << lane) - 1u;
     uint32_t nfail = 0;        // candidates whose first Marsaglia try (pair block) was rejected
+#if DSMC_OWNMAP
+    // owner of each candidate of the pass: every lane marks its cell's range (at most
+    // the cell's M entries) -- one byte load per candidate instead of a 5-step search
+    {
+      const uint32_t a0 = mst > base ? mst : base;
+      const uint32_t a1 = mst + M < base + lim ? mst + M : base + lim;
+      DSMC_LOOP_UNROLL
+      for (uint32_t k = a0; k < a1; k++) W.own[k - base] = (uint8_t)lane;
+      __syncwarp();
+    }
+#endif
     DSMC_LOOP_UNROLL
     for (uint32_t q0 = 0; q0 < lim; q0 += 64) {
       uint32_t qq[2], kq[2], nc[2];
@@ -1181,13 +1197,17 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
       for (int hh = 0; hh < 2; hh++) {
         qq[hh] = q0 + 32 * hh + lane;
         const uint32_t gq = base + qq[hh];
-        // owning cell of candidate gq: last lane with mst <= gq (binary search over lanes)
-        int lo = 0;
+        // owning cell of candidate gq: last lane with mst <= gq
+#if DSMC_OWNMAP
+        const int lo = qq[hh] < lim ? (int)W.own[qq[hh]] : 0;
+#else
+        int lo = 0;     // (binary search over lanes)
 #pragma unroll
         for (int stp = 16; stp > 0; stp >>= 1) {
           const uint32_t m = __shfl_sync(FULL, mst, lo + stp);
           if (m <= gq && lo + stp < 32) lo += stp;
         }
+#endif
         nc[hh] = __shfl_sync(FULL, N, lo);
         gq_hat[hh] = __shfl_sync(FULL, ghatu, lo);
         kq[hh] = gq - __shfl_sync(FULL, mst, lo);
@@ -1238,12 +1258,16 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
       const bool act = f0 + lane < nfail;
       const uint32_t q = act ? W.fl[f0 + lane] : 0u;
       const uint32_t gq = base + q;
+#if DSMC_OWNMAP
+      const int lo = act ? (int)W.own[q] : 0;
+#else
       int lo = 0;
 #pragma unroll
       for (int stp = 16; stp > 0; stp >>= 1) {
         const uint32_t m = __shfl_sync(FULL, mst, lo + stp);
         if (m <= gq && lo + stp < 32) lo += stp;
       }
+#endif
       const uint32_t kq = gq - __shfl_sync(FULL, mst, lo), cc = __shfl_sync(FULL, c, lo);
       const int rc = __shfl_sync(FULL, r, lo);
       if (act) {
@@ -1472,9 +1496,9 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
         const uint32_t lim = tot - base < (uint32_t)CCW ? tot - base : (uint32_t)CCW;
         // two candidates per lane per pass: four independent Philox chains in flight
         if (one_run)
-          ntc_predraw<true, MODEL>(P, W, lane, base, lim, mst, N, ghatu, r, c, (uint32_t)s, run_key(P, r_first));
+          ntc_predraw<true, MODEL>(P, W, lane, base, lim, mst, M, N, ghatu, r, c, (uint32_t)s, run_key(P, r_first));
         else
-          ntc_predraw<false, MODEL>(P, W, lane, base, lim, mst, N, ghatu, r, c, (uint32_t)s, run_key(P, r_first));
+          ntc_predraw<false, MODEL>(P, W, lane, base, lim, mst, M, N, ghatu, r, c, (uint32_t)s, run_key(P, r_first));
         cp_async_wait_all();                      // the velocity gathers of D (pending in the first pass only)
         __syncwarp();
         if (Mu) {
