@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--n-runs", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-batches", type=int, default=0,
+                    help="sub-batches (contexts) the e2e leg streams the runs in (0: n/32 when n >= 64, else 1)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--timed-steps", type=int, default=4, help="steps of the per-kernel event-timed pass")
     ap.add_argument("--reorder-every", type=int, default=None, help="physical reorder period K (problem parameter)")
@@ -257,10 +259,22 @@ def run_ours(args):
         except Exception:
             pass
 
-    # end-to-end through the C ABI with host buffers: upload the batch state
-    # from pinned host memory, K steps, explicit Sampling, D2H of the macros
+    # end-to-end through the C ABI with host buffers: the batch state (positions,
+    # velocities, majorants) uploaded from pinned host memory, K steps, explicit
+    # Sampling, the one exchange, the ensemble macros to host.  The runs are
+    # independent, so the batch is streamed in B sub-batches,
+    # one context (stream, graph) each: sub-batch b+1's upload (host-synchronous on
+    # its own stream) overlaps sub-batch b's steps, and the exchange gathers the B
+    # blocks of slot sums in ascending run id -- bit-identical to one context
+    # (tests/test_gpu_parity_r2.py::test_gathered_ensemble_equals_single_context).
     e2e = None
     if not args.no_e2e:
+        # default: sub-batches of 32 runs (c4 n = 256, e2e G particle-steps/s for B = 1 / 2 / 4 / 8:
+        # 20.1 / 26.0 / 29.8 / 33.2; the PCIe upload of the state is then the critical path)
+        B = args.e2e_batches or (sim.R // 32 if sim.R >= 64 and sim.R % 32 == 0 else 1)
+        if sim.R % B:
+            B = 1
+        m = sim.R // B
         host = []
         nbytes_h2d = 0
         for r in range(sim.R):
@@ -272,26 +286,44 @@ def run_ours(args):
                 t = torch.from_numpy(s_[k]).pin_memory()
                 pinned[k] = t
                 nbytes_h2d += t.numel() * 4
-            host.append((len(s_["x"]), pinned))
+            gm = torch.from_numpy(sim.get_gmax(r)).pin_memory()
+            nbytes_h2d += gm.numel() * 4
+            host.append((len(s_["x"]), pinned, gm))
         step0 = st2[0]["step"]
+        subs = []
+        for b in range(B):
+            q = dict(p)
+            q["n_runs"] = m
+            q["run_id0"] = p["run_id0"] + b * m
+            subs.append(dsmc.Simulation(q, device=f"cuda:{local}", stream=torch.cuda.Stream(device=f"cuda:{local}")))
+        sa = [s.status()[1] for s in subs]
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        for r, (n, pin) in enumerate(host):
-            _set_state_pinned(sim, dsmc, r, n, pin, step0)
-        _, sa = sim.status()
-        sim.step(K)
-        sim.sample(0)
-        # the paper's one exchange: every rank's slot sums gathered
-        # in run order (NCCL all-gather; one block on one GPU), then the ensemble
-        macros = runs.ensemble_over_ranks(sim, 0)
+        for b, s in enumerate(subs):
+            for j in range(m):
+                n, pin, gm = host[b * m + j]
+                _set_state_pinned(s, dsmc, j, n, pin, step0, gm)
+            s.step(K)
+        for s in subs:
+            s.sample(0)
+        torch.cuda.synchronize()                 # every sub-batch's stream
+        # the paper's one exchange: the slot sums of every sub-batch
+        # and every rank gathered in run order (NCCL all-gather), then the ensemble
+        local_sums = torch.stack([s.slot_sums_device(0) for s in subs])
+        g = runs.gather_slot_sums(local_sums).reshape(-1, *local_sums.shape[1:])
+        macros = subs[0].read_macros_gathered(0, g, g.shape[0])
         t1 = time.perf_counter()
-        _, sb = sim.status()
-        ps_e2e = sum(b["particle_steps"] - a["particle_steps"] for a, b in zip(sa, sb))
+        sb = [s.status()[1] for s in subs]
+        ps_e2e = sum(y["particle_steps"] - x["particle_steps"] for a_, b_ in zip(sa, sb) for x, y in zip(a_, b_))
         e2e_val = runs.sum_over_ranks(ps_e2e) / runs.max_over_ranks(t1 - t0)
         e2e = {"value": e2e_val, "unit": "particle-steps/s", "h2d_bytes_per_step": nbytes_h2d // K,
-               "d2h_bytes_per_step": macros.nbytes // K,
-               "what": "set_state(all runs, pinned host) + K graph steps + dsmc_sample + gather of the slot "
-                       "sums over ranks + dsmc_read_macros_gathered (macros to host)"}
+               "d2h_bytes_per_step": macros.nbytes // K, "sub_batches": B,
+               "what": f"{B} sub-batch context(s) of {m} runs: set_state + set_gmax (pinned host) of each run, "
+                       "K graph steps (sub-batch b+1's upload overlaps sub-batch b's steps), dsmc_sample, "
+                       "gather of the slot sums over sub-batches and ranks, dsmc_read_macros_gathered (macros to host)"}
+        del subs
 
     rc, _ = sim.status(raise_on_fault=False)
     cpu = None
@@ -319,12 +351,15 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def _set_state_pinned(sim, dsmc, r, n, pin, step):
-    """dsmc_set_state straight from pinned host tensors (alive = NULL)."""
+def _set_state_pinned(sim, dsmc, r, n, pin, step, gmax=None):
+    """dsmc_set_state (and dsmc_set_gmax) straight from pinned host tensors (alive = NULL)."""
     import ctypes as C
     ptr = {k: C.c_void_p(v.data_ptr()) for k, v in pin.items()}
     args = [ptr.get(k) for k in ("x", "y", "z", "vx", "vy", "vz")]
-    dsmc._check(dsmc.load_library().dsmc_set_state(sim.h, r, n, *args, None, step))
+    L = dsmc.load_library()
+    dsmc._check(L.dsmc_set_state(sim.h, r, n, *args, None, step))
+    if gmax is not None:
+        dsmc._check(L.dsmc_set_gmax(sim.h, r, C.c_void_p(gmax.data_ptr())))
 
 
 def cpu_baseline(p, budget_s=12.0):
