@@ -379,8 +379,60 @@ def cpu_baseline(p, budget_s=12.0):
         if time.perf_counter() - t0 > budget_s or steps >= configs.n_steps(p):
             break
     el = time.perf_counter() - t0
-    return {"value": ps / el, "unit": "particle-steps/s", "cores": 1, "kind": "oracle", "cpu": cpu_model(),
-            "sample": f"run {p['run_id0']} of the same workload, steps 0..{steps - 1} ({ps} particle-steps, {el:.1f} s)"}
+    out = {"value": ps / el, "unit": "particle-steps/s", "cores": 1, "kind": "oracle", "cpu": cpu_model(),
+           "sample": f"run {p['run_id0']} of the same workload, steps 0..{steps - 1} ({ps} particle-steps, {el:.1f} s)"}
+    psir = cpu_psir(p, budget_s)
+    if psir:
+        psir["speedup_vs_1"] = psir["value"] / out["value"]
+        q, S = psir["threads"], psir["speedup_vs_1"]
+        # Eq. 4 solved for the parallel fraction alpha at the measured speedup
+        psir["eq4_alpha"] = q * (1.0 - 1.0 / S) / (q - 1.0) if q > 1 else None
+        out["psir"] = psir
+    return out
+
+
+def cpu_psir(p, budget_s=12.0):
+    """the paper's first level (PSIR) on the host cores --
+    one oracle run per thread (runs run_id0 .. run_id0 + q - 1, independent), every
+    thread stepping its run for ~budget_s; the oracle's C calls release the GIL.
+    Returns the aggregate particle-steps/s, or None on a one-core host."""
+    import threading
+    from oracle import oracle
+    try:
+        q = len(os.sched_getaffinity(0))
+    except Exception:
+        q = os.cpu_count() or 1
+    if q < 2:
+        return None
+    orcs = [oracle.OracleRun(p, p["run_id0"] + t) for t in range(q)]
+    done = [0] * q
+    steps = [0] * q
+    go = threading.Barrier(q + 1)
+    t_end = [0.0]
+
+    def work(t):
+        o = orcs[t]
+        o.fill()
+        go.wait()
+        while time.perf_counter() < t_end[0] and steps[t] < configs.n_steps(p):
+            n_before = o.n
+            o.step(1)
+            done[t] += n_before
+            steps[t] += 1
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(q)]
+    for x in th:
+        x.start()
+    t_end[0] = time.perf_counter() + 1e9        # until the barrier: set below
+    go.wait()
+    t0 = time.perf_counter()
+    t_end[0] = t0 + budget_s
+    for x in th:
+        x.join()
+    el = time.perf_counter() - t0
+    return {"value": sum(done) / el, "threads": q,
+            "sample": f"runs {p['run_id0']}..{p['run_id0'] + q - 1}, one per thread, {min(steps)}-{max(steps)} "
+                      f"steps each ({sum(done)} particle-steps, {el:.1f} s)"}
 
 
 def run_reference(args):
