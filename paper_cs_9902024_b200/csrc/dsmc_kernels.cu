@@ -879,6 +879,9 @@ __device__ __forceinline__ void pair_of(uint32_t w, uint32_t N, uint32_t& i, uin
 #ifndef DSMC_WALK_UNROLL_N
 #define DSMC_WALK_UNROLL_N 1   // 0: the compiler's choice
 #endif
+#ifndef DSMC_CCARITH
+#define DSMC_CCARITH 1         // E1 takes a one-run tile's owner cell as c(lane 0) + owner, not by a shuffle
+#endif                         // (c4 k_collide 9.82 -> 9.78-9.79 ms; 0: the shuffle, A/B)
 struct SmemCell4 {          // shared-memory cell, velocities as float4 (x, y, z, -): one LDS.128 / STS.128
   float4* v;
   __device__ void ld(uint32_t i, float a[3]) const { const float4 t = v[i]; a[0] = t.x; a[1] = t.y; a[2] = t.z; }
@@ -1176,6 +1179,7 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
                                             uint32_t s, uint2 key_u) {
     const unsigned lt = (1u << lane) - 1u;
     uint32_t nfail = 0;        // candidates whose first Marsaglia try (pair block) was rejected
+    const uint32_t c0 = (UK && DSMC_CCARITH) ? __shfl_sync(FULL, c, 0) : 0u;   // one run: c(lane) = c0 + lane
 #if DSMC_OWNMAP
     // owner of each candidate of the pass: every lane marks its cell's range (at most
     // the cell's M entries) -- one byte load per candidate instead of a 5-step search
@@ -1212,7 +1216,7 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
         gq_hat[hh] = __shfl_sync(FULL, ghatu, lo);
         kq[hh] = gq - __shfl_sync(FULL, mst, lo);
         rc[hh] = __shfl_sync(FULL, r, lo);
-        cc[hh] = __shfl_sync(FULL, c, lo);
+        cc[hh] = (UK && DSMC_CCARITH) ? c0 + (uint32_t)lo : __shfl_sync(FULL, c, lo);
       }
       uint4 wp[2];
 #pragma unroll
@@ -1268,7 +1272,8 @@ __device__ __forceinline__ void ntc_predraw(const Prm& P, const WarpSmem& W, int
         if (m <= gq && lo + stp < 32) lo += stp;
       }
 #endif
-      const uint32_t kq = gq - __shfl_sync(FULL, mst, lo), cc = __shfl_sync(FULL, c, lo);
+      const uint32_t kq = gq - __shfl_sync(FULL, mst, lo);
+      const uint32_t cc = (UK && DSMC_CCARITH) ? c0 + (uint32_t)lo : __shfl_sync(FULL, c, lo);
       const int rc = __shfl_sync(FULL, r, lo);
       if (act) {
         const uint2 keyc = UK ? key_u : run_key(P, rc);

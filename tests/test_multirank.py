@@ -57,11 +57,14 @@ def _worker(rank, world, port, out_path):
     dist.destroy_process_group()
 
 
-def _worker_slot_layout(rank, world, port, out_path):
+def _worker_slot_layout(rank, world, port, out_path, sub=1):
     """The exchange in the product's layout: each rank's slot sums as dsmc_read_sums /
     Simulation.slot_sums_device lay them out, [5][n_local*Nc], gathered into
     [world][5][n_local*Nc] by runs.gather_slot_sums (the input of
-    dsmc_read_macros_gathered)."""
+    dsmc_read_macros_gathered).  sub > 1: the rank holds its runs in `sub`
+    sub-batch contexts (bench.py's e2e leg), their slot sums stacked
+    [sub][5][n_local/sub*Nc] before the gather and the result read as
+    world*sub blocks."""
     sys.path.insert(0, ROOT)
     import torch
     import torch.distributed as dist
@@ -82,23 +85,28 @@ def _worker_slot_layout(rank, world, port, out_path):
         o.fill()
         o.step(20)
         snaps.append(o.get_snap(0))                                    # [5][Nc]
-    local = torch.from_numpy(np.array(snaps).transpose(1, 0, 2).reshape(5, 3 * Nc).copy())
+    m = 3 // sub
+    blocks = [np.array(snaps[b * m:(b + 1) * m]).transpose(1, 0, 2).reshape(5, m * Nc) for b in range(sub)]
+    local = torch.from_numpy(np.array(blocks[0] if sub == 1 else blocks).copy())
     g = runs.gather_slot_sums(local)
-    assert tuple(g.shape) == (world, 5, 3 * Nc)
+    assert tuple(g.shape) == ((world, 5, 3 * Nc) if sub == 1 else (world, sub, 5, m * Nc))
+    g = g.reshape(-1, 5, m * Nc)                                       # world*sub blocks in run order
     if rank == 0:
-        per_run = g.numpy().reshape(world, 5, 3, Nc).transpose(0, 2, 1, 3).reshape(world * 3, 5, Nc)
+        per_run = g.numpy().reshape(world * sub, 5, m, Nc).transpose(0, 2, 1, 3).reshape(world * 3, 5, Nc)
         np.savez(out_path, ens=oracle.ensemble(per_run, job["fnum_vc"]), per_run=per_run)
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_two_rank_gather_in_product_layout(tmp_path, oracle_mod):
+@pytest.mark.parametrize("sub", [1, 3])
+def test_two_rank_gather_in_product_layout(tmp_path, oracle_mod, sub):
     """runs.gather_slot_sums over gloo, world size 2: block k of the gathered tensor is
     rank k's slot, so the runs come out in ascending global id and the ensemble of
-    the gathered sums equals the single-process ensemble over all 6 runs bit for bit."""
+    the gathered sums equals the single-process ensemble over all 6 runs bit for bit
+    (sub = 3: each rank's runs in three sub-batch contexts, as bench.py's e2e leg)."""
     from workloads import configs
     out = str(tmp_path / "g0.npz")
-    mp.spawn(_worker_slot_layout, args=(2, _free_port(), out), nprocs=2, join=True)
+    mp.spawn(_worker_slot_layout, args=(2, _free_port(), out, sub), nprocs=2, join=True)
     got = np.load(out)
     job = configs.get("c2_small", n_runs=6, n_steps=20)
     sums = []
