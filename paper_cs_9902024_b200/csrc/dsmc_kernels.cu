@@ -882,10 +882,16 @@ __device__ __forceinline__ void pair_of(uint32_t w, uint32_t N, uint32_t& i, uin
 #ifndef DSMC_CCARITH
 #define DSMC_CCARITH 1         // E1 takes a one-run tile's owner cell as c(lane 0) + owner, not by a shuffle
 #endif                         // (c4 k_collide 9.82 -> 9.78-9.79 ms; 0: the shuffle, A/B)
-struct SmemCell4 {          // shared-memory cell, velocities as float4 (x, y, z, -): one LDS.128 / STS.128
-  float4* v;
-  __device__ void ld(uint32_t i, float a[3]) const { const float4 t = v[i]; a[0] = t.x; a[1] = t.y; a[2] = t.z; }
-  __device__ void st(uint32_t i, const float a[3]) const { v[i] = make_float4(a[0], a[1], a[2], 0.0f); }
+// k_collide's staged cell: velocities as 3 floats per particle (12-byte stride: lane-strided
+// LDS.32 are conflict-free).  float4 (one LDS.128 per particle) costs 4 more bytes per staged
+// particle, and the kernel's speed follows the L1 its shared memory leaves: at c4 the 16 one-warp
+// blocks of an SM then need 190 KB (196 KB carveout, 60 KB of L1) against 160 KB (164 KB carveout,
+// 92 KB of L1): k_collide 9.80 -> 8.93 ms at n = 256 (float3 under a forced 196 KB carveout: 9.62)
+constexpr int VS = 3;       // floats per staged velocity
+struct SmemCellV {
+  float* v;
+  __device__ void ld(uint32_t i, float a[3]) const { a[0] = v[3 * i]; a[1] = v[3 * i + 1]; a[2] = v[3 * i + 2]; }
+  __device__ void st(uint32_t i, const float a[3]) const { v[3 * i] = a[0]; v[3 * i + 1] = a[1]; v[3 * i + 2] = a[2]; }
 };
 struct SmemCell {
   float* vx; float* vy; float* vz; uint8_t* mod;
@@ -1142,8 +1148,8 @@ constexpr int CCW = DSMC_CCW;   // pre-drawn candidates per round per warp
 
 struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
   uint32_t* sorted;         // [capw] canonical (sorted) store indices of the tile
-  uint32_t* a;              // [capw + APAD] the staged LCR slice (aliases v4: dead after phase C)
-  float4* v4;               // [capw] velocities (x, y, z, -) in canonical order
+  uint32_t* a;              // [capw + APAD] the staged LCR slice (aliases vf: dead after phase C)
+  float* vf;                // [capw][VS] velocities (x, y, z) in canonical order
   float4* rec;              // [CCW] pre-drawn candidate: unit vector (R14) and acceptance threshold / word
   uint32_t* cij;            // [CCW] candidate pair i | j << 16
   uint8_t* cell; uint8_t* fl;
@@ -1151,21 +1157,25 @@ struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
 };
 
 // the staged LCR slice `a` (the bulk copy's 16-byte aligned window around [S, E): up
-// to 3 words of slack on either side) aliases the 16 capw bytes of v4
-__host__ __device__ inline size_t warp_smem_bytes(int capw) {   // capw a multiple of 32
-  return (size_t)capw * (4 + 16 + 1) + (size_t)CCW * (16 + 4 + 1 + (DSMC_OWNMAP ? 1 : 0)) + 16;
+// to 3 words of slack on either side) aliases the 12 capw bytes of vf
+// `one`: every tile of the kernel lies in one run (ONE): the tags are then used by the rank
+// sort of C only and can share the records' bytes (capw <= 16 CCW is checked by the host)
+__host__ __device__ inline bool cell_aliased(int capw, bool one) { return one && capw <= 16 * CCW; }
+__host__ __device__ inline size_t warp_smem_bytes(int capw, bool one) {   // capw a multiple of 32
+  return (size_t)capw * (4 + 4 * VS + (cell_aliased(capw, one) ? 0 : 1)) +
+         (size_t)CCW * (16 + 4 + 1 + (DSMC_OWNMAP ? 1 : 0)) + 16;
 }
 
-__device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw) {
+__device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int capw, bool one) {
   WarpSmem w;
   w.sorted = reinterpret_cast<uint32_t*>(base);
-  w.v4 = reinterpret_cast<float4*>(w.sorted + capw);        // 16-byte aligned (capw % 4 == 0)
-  w.a = reinterpret_cast<uint32_t*>(w.v4);                   // 4 capw + APAD words fit in 16 capw bytes
-  w.rec = w.v4 + capw;
+  w.vf = reinterpret_cast<float*>(w.sorted + capw);          // 16-byte aligned (capw % 4 == 0)
+  w.a = reinterpret_cast<uint32_t*>(w.vf);                   // capw + APAD words fit in 3 capw words
+  w.rec = reinterpret_cast<float4*>(w.vf + (size_t)VS * capw);
   w.cij = reinterpret_cast<uint32_t*>(w.rec + CCW);
-  w.cell = reinterpret_cast<uint8_t*>(w.cij + CCW);
-  w.fl = w.cell + capw;      // candidates whose first Marsaglia try was rejected
+  w.fl = reinterpret_cast<uint8_t*>(w.cij + CCW);      // candidates whose first Marsaglia try was rejected
   w.own = w.fl + CCW;
+  w.cell = cell_aliased(capw, one) ? reinterpret_cast<uint8_t*>(w.rec) : w.own + CCW;
   return w;
 }
 
@@ -1448,7 +1458,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
     }
     __syncwarp();
     // ---- D
-    float4* const v4 = W.v4;
+    float* const vf = W.vf;
     if (one_run) {
       // per-array base pointers indexed by 32-bit offsets (one IMAD.WIDE per access)
       const float* __restrict__ sx = (h ? P1 : P0) + 3 * RS;
@@ -1460,7 +1470,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
       DSMC_LANE_UNROLL
       for (uint32_t q = lane; q < cnt; q += 32) {
         const uint32_t g = W.sorted[q];
-        float* d = reinterpret_cast<float*>(v4 + q);
+        float* d = vf + VS * q;
         cp_async4(d, sx + g);
         cp_async4(d + 1, sy + g);
         cp_async4(d + 2, sz + g);
@@ -1483,7 +1493,9 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
 #pragma unroll
             for (int a = 0; a < D; a++) d[a * RS] = src[a * RS];
           }
-          v4[q] = make_float4(src[3 * RS], src[4 * RS], src[5 * RS], 0.0f);
+          vf[VS * q] = src[3 * RS];
+          vf[VS * q + 1] = src[4 * RS];
+          vf[VS * q + 2] = src[5 * RS];
         }
       }
     }
@@ -1493,7 +1505,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
       ncand = M;
       const uint32_t Mu = M, mstu = mst;
       const double gmu = (double)gm, ghatu = gmu / P.sigma_c;
-      SmemCell4 Au{v4 + off};
+      SmemCellV Au{vf + VS * off};
       float maxg2 = 0.0f;
       uint32_t naccu = 0;
       DSMC_LOOP_UNROLL
@@ -1523,7 +1535,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
     }
     cp_async_wait_all();                          // no candidates (or no Interaction): gathers of D
     __syncwarp();
-    if (valid && slot >= 0) sample_cell(P, slot, k, N, SmemCell4{v4 + off}, mode == 2);
+    if (valid && slot >= 0) sample_cell(P, slot, k, N, SmemCellV{vf + VS * off}, mode == 2);
     // a tile without an accepted collision changed no velocity: nothing to write back
     // on a non-reorder step (sparse tiles, e.g. c5's background)
     const bool any_acc = __any_sync(FULL, nacc != 0);
@@ -1539,10 +1551,11 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
         float* __restrict__ dz = dy + RS;
         DSMC_LANE_UNROLL
         for (uint32_t q = lane; q < cnt; q += 32) {
-          const float4 v = v4[q];
-          dx[3 * RS + q] = v.x;
-          dy[3 * RS + q] = v.y;
-          dz[3 * RS + q] = v.z;
+          float v[3];
+          SmemCellV{vf}.ld(q, v);
+          dx[3 * RS + q] = v[0];
+          dy[3 * RS + q] = v[1];
+          dz[3 * RS + q] = v[2];
         }
         __syncwarp();
         const float* __restrict__ px = (h ? P1 : P0);
@@ -1551,7 +1564,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
         DSMC_LANE_UNROLL
         for (uint32_t q = lane; q < cnt; q += 32) {
           const uint32_t g = W.sorted[q];
-          float* d = reinterpret_cast<float*>(v4 + q);
+          float* d = vf + VS * q;
           cp_async4(d, px + g);
           if (D > 1) cp_async4(d + 1, py + g);
           if (D > 2) cp_async4(d + 2, pz + g);
@@ -1561,10 +1574,11 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
         __syncwarp();
         DSMC_LANE_UNROLL
         for (uint32_t q = lane; q < cnt; q += 32) {
-          const float4 v = v4[q];
-          dx[q] = v.x;
-          if (D > 1) dy[q] = v.y;
-          if (D > 2) dz[q] = v.z;
+          float v[3];
+          SmemCellV{vf}.ld(q, v);
+          dx[q] = v[0];
+          if (D > 1) dy[q] = v[1];
+          if (D > 2) dz[q] = v[2];
         }
       } else if (any_acc) {
         float* __restrict__ vxp = (h ? P1 : P0) + 3 * RS;
@@ -1573,10 +1587,11 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
         DSMC_LANE_UNROLL
         for (uint32_t q = lane; q < cnt; q += 32) {
           const uint32_t g = W.sorted[q];
-          const float4 v = v4[q];
-          vxp[g] = v.x;
-          vyp[g] = v.y;
-          vzp[g] = v.z;
+          float v[3];
+          SmemCellV{vf}.ld(q, v);
+          vxp[g] = v[0];
+          vyp[g] = v[1];
+          vzp[g] = v[2];
         }
       }
     } else {
@@ -1590,16 +1605,18 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
         if (q < cnt) {
           if (rq) {
             float* d = (hq ? P0 : P1) + (int64_t)runq * P.stride + (int64_t)(S + q - bq);
-            const float4 v = v4[q];
-            d[3 * RS] = v.x;
-            d[4 * RS] = v.y;
-            d[5 * RS] = v.z;
+            float v[3];
+            SmemCellV{vf}.ld(q, v);
+            d[3 * RS] = v[0];
+            d[4 * RS] = v[1];
+            d[5 * RS] = v[2];
           } else {                               // full write-back (no collided flags)
             float* d = (hq ? P1 : P0) + W.sorted[q];
-            const float4 v = v4[q];
-            d[3 * RS] = v.x;
-            d[4 * RS] = v.y;
-            d[5 * RS] = v.z;
+            float v[3];
+            SmemCellV{vf}.ld(q, v);
+            d[3 * RS] = v[0];
+            d[4 * RS] = v[1];
+            d[5 * RS] = v[2];
           }
         }
       }
@@ -1638,7 +1655,7 @@ __global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, 
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ __align__(8) uint64_t s_bar;        // completion of the LCR slice's bulk copy (WPB == 1)
   const int wid = threadIdx.x >> 5;
-  const WarpSmem W = warp_smem(dsm + (size_t)wid * warp_smem_bytes(capw), capw);
+  const WarpSmem W = warp_smem(dsm + (size_t)wid * warp_smem_bytes(capw, ONE), capw, ONE);
   uint32_t ph = 0;
   collide_tile<D, NET, MODEL, STEP, ONE, false>(P, mode_arg, slot_arg, capw, W, &s_bar, ph,
                                                 ((int64_t)blockIdx.x * WPB + wid) * 32);
@@ -1732,7 +1749,7 @@ template <int D, int NET, int MODEL, bool ONE>
 __global__ void __launch_bounds__(32, DSMC_COLLIDE_MINB) k_collide_list(Prm P, int capw) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ __align__(8) uint64_t s_bar;
-  const WarpSmem W = warp_smem(dsm, capw);
+  const WarpSmem W = warp_smem(dsm, capw, ONE);
   if (threadIdx.x == 0) mbar_init(&s_bar, 1u);
   __syncwarp();
   uint32_t ph = 0;
@@ -2381,7 +2398,7 @@ static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t s
   const int64_t RN = (int64_t)P.R * P.Nc;
   const int64_t warps = (RN + 31) / 32;
   const unsigned g = (unsigned)((warps + WPB - 1) / WPB);
-  const size_t smem = WPB * warp_smem_bytes(capw);
+  const size_t smem = WPB * warp_smem_bytes(capw, ONE);
   static size_t configured_dev[MAX_DEV] = {0};
   size_t& configured = configured_dev[cur_dev()];
   if (smem > configured) {
@@ -2395,7 +2412,7 @@ static void collide_t(const Prm& P, int mode, int slot, int capw, cudaStream_t s
 
 template <int D, int NET, int MODEL, bool ONE>
 static void collide_list_t(const Prm& P, int capw, cudaStream_t st) {
-  const size_t smem = warp_smem_bytes(capw);
+  const size_t smem = warp_smem_bytes(capw, ONE);
   static size_t configured_dev[MAX_DEV] = {0};
   static int occ_dev[MAX_DEV] = {0};
   const int dev = cur_dev();
