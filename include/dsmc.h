@@ -34,7 +34,7 @@
  *   - Thread safety: a dsmc_ctx is used by one host thread at a time.
  *   - Environment switches read by dsmc_create (measurement A/B only; results are
  *     bit-identical with or without them): DSMC_STATIC_CELLS=1 disables the
- *     heavy-tile queue (static lane-per-cell mapping, NEXT-1); DSMC_CAPW=<n>
+ *     heavy-tile queue (static block-per-tile mapping, NEXT-1); DSMC_CAPW=<n>
  *     overrides the warp-tile staging capacity; DSMC_CARVEOUT=<percent> sets the
  *     collide kernel's preferred shared-memory carveout; DSMC_COMPACT=0/1 forces
  *     the sparse-problem tile list (k_collide_triage) off or on; DSMC_NO_BRANCH=1

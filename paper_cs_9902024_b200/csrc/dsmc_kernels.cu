@@ -888,6 +888,12 @@ __device__ __forceinline__ void pair_of(uint32_t w, uint32_t N, uint32_t& i, uin
 // blocks of an SM then need 190 KB (196 KB carveout, 60 KB of L1) against 160 KB (164 KB carveout,
 // 92 KB of L1): k_collide 9.80 -> 8.93 ms at n = 256 (float3 under a forced 196 KB carveout: 9.62)
 constexpr int VS = 3;       // floats per staged velocity
+// k_collide reads its cell data (ends, majorant) once and writes velocities and positions it
+// never reads again: streaming loads / stores (evict-first) keep them from displacing the
+// sectors the gathers share in L1 and L2 (c4 n = 256: k_collide 8.94 -> 8.79 ms; loads alone
+// 8.93, stores alone 8.82)
+#define DSMC_LD1(p) __ldcs(p)
+#define DSMC_ST1(p, v) __stcs(p, v)
 struct SmemCellV {
   float* v;
   __device__ void ld(uint32_t i, float a[3]) const { a[0] = v[3 * i]; a[1] = v[3 * i + 1]; a[2] = v[3 * i + 2]; }
@@ -1342,8 +1348,8 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
   // ---- A
   uint32_t st = 0, en = 0;
   if (valid) {
-    st = k == 0 ? 0u : P.cell[k - 1];
-    en = P.cell[k];
+    st = k == 0 ? 0u : DSMC_LD1(P.cell + k - 1);
+    en = DSMC_LD1(P.cell + k);
   }
   const int r = ONE ? r_first : (valid ? (int)run_of(P, (uint32_t)k) : r_last);
   const uint32_t c = valid ? (uint32_t)k - (uint32_t)r * Nc32 : 0u;
@@ -1380,7 +1386,7 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
     }
     return;
   }
-  float gm = valid ? P.gmax[k] : 0.0f;
+  float gm = valid ? DSMC_LD1(P.gmax + k) : 0.0f;
   const float gm0 = gm;
   {
     // ---- B: the tile's LCR slice [S, E) is contiguous: one lane moves its 16-byte
@@ -1553,9 +1559,9 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
         for (uint32_t q = lane; q < cnt; q += 32) {
           float v[3];
           SmemCellV{vf}.ld(q, v);
-          dx[3 * RS + q] = v[0];
-          dy[3 * RS + q] = v[1];
-          dz[3 * RS + q] = v[2];
+          DSMC_ST1(dx + 3 * RS + q, v[0]);
+          DSMC_ST1(dy + 3 * RS + q, v[1]);
+          DSMC_ST1(dz + 3 * RS + q, v[2]);
         }
         __syncwarp();
         const float* __restrict__ px = (h ? P1 : P0);
@@ -1576,9 +1582,9 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
         for (uint32_t q = lane; q < cnt; q += 32) {
           float v[3];
           SmemCellV{vf}.ld(q, v);
-          dx[q] = v[0];
-          if (D > 1) dy[q] = v[1];
-          if (D > 2) dz[q] = v[2];
+          DSMC_ST1(dx + q, v[0]);
+          if (D > 1) DSMC_ST1(dy + q, v[1]);
+          if (D > 2) DSMC_ST1(dz + q, v[2]);
         }
       } else if (any_acc) {
         float* __restrict__ vxp = (h ? P1 : P0) + 3 * RS;
@@ -1589,9 +1595,9 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
           const uint32_t g = W.sorted[q];
           float v[3];
           SmemCellV{vf}.ld(q, v);
-          vxp[g] = v[0];
-          vyp[g] = v[1];
-          vzp[g] = v[2];
+          DSMC_ST1(vxp + g, v[0]);
+          DSMC_ST1(vyp + g, v[1]);
+          DSMC_ST1(vzp + g, v[2]);
         }
       }
     } else {
@@ -2537,7 +2543,11 @@ static void heavy_q(const Prm& P, int mode, int slot, int q, cudaStream_t st) {
 // blocks per SM; tiles beyond the last tier take its global-memory path
 void launch_collide_heavy(const Prm& P, int mode, int slot, cudaStream_t st) {
   if (!P.heavy_list) return;
-  for (int q = 0; q < HEAVY_TIERS; q++) {
+  // the large tier first: beside the warp-tile list (second graph branch) its one block per
+  // SM leaves the list room, and the small tier's finer blocks make the shorter tail
+  // (c5 after 500 steps: 1.858 -> 1.822 ms per step; c2 0.307 -> 0.311); a graph branch per
+  // tier changed nothing (c5 1.857 -> 1.865): the tiers' 96-193 KB blocks cannot share an SM
+  for (int q = HEAVY_TIERS - 1; q >= 0; q--) {
     if (P.dim == 1) heavy_q<1>(P, mode, slot, q, st);
     else if (P.dim == 2) heavy_q<2>(P, mode, slot, q, st);
     else heavy_q<3>(P, mode, slot, q, st);
