@@ -1149,7 +1149,10 @@ __device__ void heap_sort(uint32_t* a, uint32_t n) {
 //   F  write modified velocities back (or the whole tile to its new rank)
 // mode 0: full step; mode 1: sample only into `slot_arg` (dsmc_sample);
 // mode 2: sample added to `slot_arg` (dsmc_sample_add, time averaging).
-constexpr int WPB = 1;      // warps per block (1: the tile index, hence run and key, is uniform)
+#ifndef DSMC_WPB
+#define DSMC_WPB 1
+#endif
+constexpr int WPB = DSMC_WPB;   // warps per block (1: the tile index, hence run and key, is uniform)
 constexpr int CCW = DSMC_CCW;   // pre-drawn candidates per round per warp
 
 struct WarpSmem {           // carve-out of one warp's slice of dynamic smem
@@ -1657,9 +1660,10 @@ __device__ __forceinline__ void collide_tile(const Prm& P, const int mode_arg, c
 }
 
 template <int D, int NET, int MODEL, bool STEP, bool ONE>
-__global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB) k_collide(Prm P, int mode_arg, int slot_arg, int capw) {
+__global__ void __launch_bounds__(WPB * 32, DSMC_COLLIDE_MINB / WPB) k_collide(Prm P, int mode_arg, int slot_arg, int capw) {
   extern __shared__ __align__(16) uint8_t dsm[];
-  __shared__ __align__(8) uint64_t s_bar;        // completion of the LCR slice's bulk copy (WPB == 1)
+  __shared__ __align__(8) uint64_t s_bars[WPB];  // completion of each warp's bulk copy of its LCR slice
+  uint64_t& s_bar = s_bars[threadIdx.x >> 5];
   const int wid = threadIdx.x >> 5;
   const WarpSmem W = warp_smem(dsm + (size_t)wid * warp_smem_bytes(capw, ONE), capw, ONE);
   uint32_t ph = 0;
