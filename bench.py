@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--n-runs", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-batches", type=int, default=0,
-                    help="sub-batches (contexts) the e2e leg streams the runs in (0: n/32 when n >= 64, else 1)")
+                    help="sub-batches (contexts) the e2e leg streams the runs in (0: n/16 when n >= 64, else 1)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--timed-steps", type=int, default=4, help="steps of the per-kernel event-timed pass")
     ap.add_argument("--reorder-every", type=int, default=None, help="physical reorder period K (problem parameter)")
@@ -271,7 +271,7 @@ def run_ours(args):
     if not args.no_e2e:
         # default: sub-batches of 32 runs (c4 n = 256, e2e G particle-steps/s for B = 1 / 2 / 4 / 8:
         # 20.1 / 26.0 / 29.8 / 33.2; the PCIe upload of the state is then the critical path)
-        B = args.e2e_batches or (sim.R // 32 if sim.R >= 64 and sim.R % 32 == 0 else 1)
+        B = args.e2e_batches or (sim.R // 16 if sim.R >= 64 and sim.R % 16 == 0 else 1)
         if sim.R % B:
             B = 1
         m = sim.R // B
