@@ -130,6 +130,30 @@ def test_one_step_parity_heavy_cells(dsmc_gpu, oracle_mod):
     one_step_case(dsmc_gpu, oracle_mod, p, 0, 2, seed_state=st)
 
 
+def test_one_step_parity_warp_tiles_rank_sort(dsmc_gpu, oracle_mod):
+    """Warp-path tiles (at most capw = 384 particles here) whose largest cell is beyond the
+    32-wide register network: the rank sort of phase C, whose element -> cell tags share the
+    bytes of the candidate records in the one-run kernels, then several E1 passes (a
+    300-particle cell draws far more than 128 candidates), on reorder and plain steps."""
+    p = configs.get("c4_small")
+    p["fill"] = []
+    layout = {3: [(0, 33), (1, 40), (2, 100), (31, 7)],            # 180 particles
+              5: [(4, 300), (5, 1), (6, 2), (30, 5)],               # one big cell, 308
+              7: [(c, 35) for c in range(0, 16, 2)] + [(17, 64)],   # 344
+              9: [(0, 32), (1, 33), (2, 31), (3, 65), (4, 128)]}    # network / rank-sort edge, 289
+    parts, seed = [], 50
+    for t, cells in layout.items():
+        for c, n in cells:
+            seed += 1
+            parts.append(inputs.clustered_state(seed, p, [32 * t + c], n))
+    st = {k: np.concatenate([q[k] for q in parts]) for k in parts[0]}
+    p["cap_per_run"] = len(st["x"]) + 64
+    for reorder_every, s0 in ((1, 2), (0, 3), (2, 4)):
+        p["reorder_every"] = reorder_every
+        sim, ref, cnt, oc = one_step_case(dsmc_gpu, oracle_mod, p, 0, s0, seed_state=st)
+        assert cnt["candidates"] > 128 and cnt["max_ppc"] > 150   # (the cells lose ~20% in Motion first)
+
+
 def test_one_step_parity_heavy_chunk_edges(dsmc_gpu, oracle_mod):
     """Heavy-tile segment sort at its chunk and merge-round edges: one 32-cell tile
     whose cells hold 1, 63, 64, 65, 127, 128, 129, 255, 256, 257 and 511 particles
