@@ -748,6 +748,11 @@ __global__ void k_step_end(Prm P, int mode, int slot) {
 // LCR[start[key] + rank] = global store index; warp-aggregated cursors over
 // lane-contiguous particles (same chunking as k_motion); the four atomics of
 // a chunk are issued before any result is consumed.
+#ifdef DSMC_SCATTER_LDCS          // A/B: the keys (read once) by streaming loads
+#define DSMC_LDK(p) __ldcs(p)
+#else
+#define DSMC_LDK(p) (*(p))
+#endif
 __global__ void __launch_bounds__(256) k_scatter(Prm P) {
   const int lane = threadIdx.x & 31;
   constexpr int SL = 2;      // 32-particle slices per warp iteration (returning atomics in flight)
@@ -769,7 +774,7 @@ __global__ void __launch_bounds__(256) k_scatter(Prm P) {
 #pragma unroll
     for (int j = 0; j < SL; j++) {
       const int64_t i = i0w + j * 32 + lane;
-      kn[j] = i < iend ? K[i] : DEAD_KEY;
+      kn[j] = i < iend ? DSMC_LDK(K + i) : DEAD_KEY;
     }
     for (; i0w < iend; i0w += 256 * SL) {
     uint32_t kk[SL], m[SL], p0[SL];
@@ -779,7 +784,7 @@ __global__ void __launch_bounds__(256) k_scatter(Prm P) {
 #pragma unroll
       for (int j = 0; j < SL; j++) {
         const int64_t i = i0w + 256 * SL + j * 32 + lane;
-        kn[j] = i < iend ? K[i] : DEAD_KEY;
+        kn[j] = i < iend ? DSMC_LDK(K + i) : DEAD_KEY;
       }
     }
 #pragma unroll
